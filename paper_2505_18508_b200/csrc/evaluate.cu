@@ -1,0 +1,150 @@
+// evaluate.cu -- exact cut / energy evaluator (evaluate.py:35-49), torus weight
+// generation (instances.py:203-224) and the multi-GPU best-key helper.
+#include <cstdint>
+
+#include "gsb_device.cuh"
+#include "gsb_internal.h"
+
+namespace gsb {
+
+__device__ __forceinline__ int get_bit(const uint8_t *__restrict__ b, int x) {
+  return (b[x >> 3] >> (7 - (x & 7))) & 1;
+}
+
+// grid (blocks_per_trial, T); every site contributes its right and down edge
+__global__ void torus_cut_energy_kernel(int rows, int cols, const int8_t *__restrict__ w,
+                                        const uint8_t *__restrict__ bits, int nbytes,
+                                        unsigned long long *cut, unsigned long long *energy) {
+  const int n = rows * cols;
+  const uint8_t *b = bits + (size_t)blockIdx.y * nbytes;
+  long long c = 0, e = 0;
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+    int r = x / cols, cc = x - r * cols;
+    int right = r * cols + (cc + 1 == cols ? 0 : cc + 1);
+    int down = (r + 1 == rows ? 0 : r + 1) * cols + cc;
+    int sx = get_bit(b, x), sr = get_bit(b, right), sd = get_bit(b, down);
+    int wr = w[2 * x], wd = w[2 * x + 1];
+    if (sx != sr) c += wr;
+    if (sx != sd) c += wd;
+    e += (sx == sr) ? wr : -wr;
+    e += (sx == sd) ? wd : -wd;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(cut + blockIdx.y, (unsigned long long)c);
+    atomicAdd(energy + blockIdx.y, (unsigned long long)e);
+  }
+}
+
+__global__ void graph_cut_energy_kernel(int64_t m, const int32_t *__restrict__ eu,
+                                        const int32_t *__restrict__ ev,
+                                        const int32_t *__restrict__ ew,
+                                        const uint8_t *__restrict__ bits, int nbytes,
+                                        unsigned long long *cut, unsigned long long *energy) {
+  const uint8_t *b = bits + (size_t)blockIdx.y * nbytes;
+  long long c = 0, e = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int su = get_bit(b, eu[k]), sv = get_bit(b, ev[k]);
+    long long wk = ew[k];
+    if (su != sv) c += wk;
+    e += (su == sv) ? wk : -wk;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(cut + blockIdx.y, (unsigned long long)c);
+    atomicAdd(energy + blockIdx.y, (unsigned long long)e);
+  }
+}
+
+int torus_cut_energy(int rows, int cols, const int8_t *w, const uint8_t *bits, int T,
+                     int64_t *cut, int64_t *energy, cudaStream_t stream) {
+  if (T <= 0) return GSB_OK;
+  int n = rows * cols;
+  if (cudaMemsetAsync(cut, 0, sizeof(int64_t) * T, stream) != cudaSuccess ||
+      cudaMemsetAsync(energy, 0, sizeof(int64_t) * T, stream) != cudaSuccess)
+    return set_error(GSB_ECUDA, "memset failed");
+  int bx = (n + 255) / 256;
+  if (bx > 1024) bx = 1024;
+  dim3 grid(bx, T);
+  torus_cut_energy_kernel<<<grid, 256, 0, stream>>>(rows, cols, w, bits, (n + 7) / 8,
+                                                    (unsigned long long *)cut,
+                                                    (unsigned long long *)energy);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
+}
+
+int graph_cut_energy(const gsb_graph *g, const uint8_t *bits, int T, int64_t *cut,
+                     int64_t *energy, cudaStream_t stream) {
+  if (T <= 0) return GSB_OK;
+  if (cudaMemsetAsync(cut, 0, sizeof(int64_t) * T, stream) != cudaSuccess ||
+      cudaMemsetAsync(energy, 0, sizeof(int64_t) * T, stream) != cudaSuccess)
+    return set_error(GSB_ECUDA, "memset failed");
+  int64_t bx = (g->m + 255) / 256;
+  if (bx > 1024) bx = 1024;
+  if (bx < 1) bx = 1;
+  dim3 grid((unsigned)bx, T);
+  graph_cut_energy_kernel<<<grid, 256, 0, stream>>>(g->m, g->eu_dev, g->ev_dev, g->ew_dev, bits,
+                                                    (g->n + 7) / 8, (unsigned long long *)cut,
+                                                    (unsigned long long *)energy);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
+}
+
+// weight k = 2*bit31(next32 #k) - 1; next32 #k is the low (k even) or high
+// (k odd) half of PCG64 output k>>1.  Thread i owns outputs [i*L, (i+1)*L).
+__global__ void torus_weights_kernel(u128 s0, u128 inc, int64_t nout, int64_t L,
+                                     int8_t *__restrict__ w) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t first = i * L;
+  if (first >= nout) return;
+  u128 A, C;
+  pcg_jump_coeffs((uint64_t)first, inc, A, C);
+  u128 s = A * s0 + C;
+  int64_t last = first + L < nout ? first + L : nout;
+  const u128 M = pcg_mult();
+  for (int64_t o = first; o < last; o++) {
+    s = s * M + inc;
+    uint64_t x = pcg_out(s);
+    w[2 * o] = (x >> 31) & 1 ? 1 : -1;
+    w[2 * o + 1] = (x >> 63) ? 1 : -1;
+  }
+}
+
+int torus_weights(int rows, int cols, uint64_t seed, int8_t *w, cudaStream_t stream) {
+  u128 s0, inc;
+  pcg_seed(seed, s0, inc);
+  int64_t n = (int64_t)rows * cols;
+  int64_t nout = n;  // 2n weights = n outputs
+  int64_t L = 64;
+  int64_t threads = (nout + L - 1) / L;
+  int64_t blocks = (threads + 255) / 256;
+  torus_weights_kernel<<<(unsigned)blocks, 256, 0, stream>>>(s0, inc, nout, L, w);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
+}
+
+__global__ void best_key_kernel(const int64_t *cut, int T, int64_t first, int64_t *key) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) {
+    uint64_t idx = (uint64_t)(first + t);
+    key[t] = (int64_t)(((uint64_t)cut[t] << 32) | (0xFFFFFFFFull - (idx & 0xFFFFFFFFull)));
+  }
+}
+
+int best_key(const int64_t *best_cut, int T, int64_t first, int64_t *key, cudaStream_t stream) {
+  if (T <= 0) return GSB_OK;
+  best_key_kernel<<<(T + 255) / 256, 256, 0, stream>>>(best_cut, T, first, key);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
+}
+
+}  // namespace gsb

@@ -1,0 +1,44 @@
+// gsb_internal.h -- internal declarations shared by the .cu files of libgsb_cuda.so
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/gsb.h"
+
+namespace gsb {
+
+int set_error(int code, const char *msg);
+int num_sms();
+
+// checkerboard engine (checker.cu)
+int checker_words(int rows, int cols, int *WPR, int *nw);
+bool checker_fits(int rows, int cols);
+int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+                const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
+                int32_t *sweeps_exec, uint8_t *best_bits, uint32_t *masks_ws, int *err_ws,
+                cudaStream_t stream);
+
+// reference-exact engine (refexact.cu)
+size_t ref_workspace_bytes(int n, int64_t m_adj, int T);
+int ref_run_torus(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+                  const uint64_t *table, int dmax, const uint64_t *seeds, int T,
+                  int64_t *best_cut, int32_t *sweeps_exec, uint8_t *best_bits, void *ws,
+                  size_t ws_bytes, int *err_ws, cudaStream_t stream);
+int ref_run_graph(const gsb_graph *g, int kind, int sweeps, const uint64_t *table, int dmax,
+                  const uint64_t *seeds, int T, int64_t *best_cut, int32_t *sweeps_exec,
+                  uint8_t *best_bits, void *ws, size_t ws_bytes, int *err_ws,
+                  cudaStream_t stream);
+
+// evaluator / generators (evaluate.cu)
+int torus_cut_energy(int rows, int cols, const int8_t *w, const uint8_t *bits, int T,
+                     int64_t *cut, int64_t *energy, cudaStream_t stream);
+int graph_cut_energy(const gsb_graph *g, const uint8_t *bits, int T, int64_t *cut,
+                     int64_t *energy, cudaStream_t stream);
+int torus_weights(int rows, int cols, uint64_t seed, int8_t *w, cudaStream_t stream);
+int best_key(const int64_t *best_cut, int T, int64_t first, int64_t *key, cudaStream_t stream);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace gsb

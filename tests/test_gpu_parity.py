@@ -1,0 +1,176 @@
+"""GPU parity: every CUDA path against the reference goldens and the CPU oracle.
+
+Bar: bit-exact (best_cut, best bitstring, sweeps_executed) -- all integer
+state, no tolerance.  All calls go through the C ABI (libgsb_cuda.so).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import MASTER, golden, hex_to_spins
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2505_18508_b200 import TorusSpec, generate_torus  # noqa: E402
+from paper_2505_18508_b200.campaign import mix_seed, mix_seeds  # noqa: E402
+from paper_2505_18508_b200.evaluate import cut_energy_batch  # noqa: E402
+from paper_2505_18508_b200.instances import ProblemInstance  # noqa: E402
+from paper_2505_18508_b200.solvers import (  # noqa: E402
+    ANNEALING,
+    ANNEALING_CHECKERBOARD,
+    GREEDY,
+    GREEDY_CHECKERBOARD,
+    SolverConfig,
+    default_config,
+    run_trials,
+)
+
+
+def test_device_weights_match_reference_digest():
+    for rec in golden("tori.json")["tori"]:
+        if rec["n"] > 4_000_000:
+            continue
+        inst = generate_torus(TorusSpec(rec["rows"], rec["cols"], rec["seed"]))
+        w = inst.device_weights("cuda").cpu().numpy()
+        assert hashlib.sha256(w.tobytes()).hexdigest() == rec["w_sha256"]
+        assert np.array_equal(w, inst.torus_weights)
+
+
+def test_device_weights_config5():
+    rec = [r for r in golden("tori.json")["tori"] if r["rows"] == 2000][0]
+    inst = generate_torus(TorusSpec(2000, 2000, 1))
+    w = inst.device_weights("cuda").cpu().numpy()
+    assert hashlib.sha256(w.tobytes()).hexdigest() == rec["w_sha256"]
+    assert int(w.astype(np.int64).sum()) == rec["total_weight"]
+
+
+def test_evaluator_matches_reference():
+    for rec in golden("tori.json")["tori"]:
+        if "evals" not in rec:
+            continue
+        inst = generate_torus(TorusSpec(rec["rows"], rec["cols"], rec["seed"]))
+        bits = np.stack([np.packbits(hex_to_spins(e["hex"], inst.n) == 1) for e in rec["evals"]])
+        cut, en = cut_energy_batch(inst, bits)
+        assert cut.cpu().tolist() == [e["cut"] for e in rec["evals"]]
+        assert en.cpu().tolist() == [e["energy"] for e in rec["evals"]]
+
+
+def test_graph_evaluator_matches_oracle(oracle):
+    for g in golden("graphs_small.json")["graphs"]:
+        inst = ProblemInstance.from_edges(g["n"], [tuple(e) for e in g["edges"]])
+        eu, ev, ew = inst.edge_arrays()
+        rng = np.random.default_rng(g["n"])
+        spins = rng.choice([-1, 1], size=(5, g["n"])).astype(np.int8)
+        cut, en = cut_energy_batch(inst, np.packbits(spins == 1, axis=1))
+        for i in range(5):
+            assert cut[i].item() == oracle.cut(eu.astype(np.int32), ev.astype(np.int32), ew, spins[i])
+            assert en[i].item() == oracle.energy(eu.astype(np.int32), ev.astype(np.int32), ew,
+                                                 spins[i])
+
+
+def _check_rows(inst, rows, kind_of):
+    by_cfg = {}
+    for r in rows:
+        key = (r["kind"], r["sweeps"], r["temp_start"], r["temp_end"])
+        by_cfg.setdefault(key, []).append(r)
+    for (kind, sweeps, t0, t1), rs in by_cfg.items():
+        cfg = SolverConfig(kind_of(kind), sweeps, 0, t0, t1)
+        b = run_trials(inst, cfg, [r["seed"] for r in rs])
+        for i, r in enumerate(rs):
+            assert int(b.best_cut[i]) == r["best_cut"], (kind, sweeps, r["seed"])
+            assert int(b.sweeps_executed[i]) == r["sweeps_executed"], (kind, sweeps, r["seed"])
+            assert b.hex(i) == r["hex"], (kind, sweeps, r["seed"])
+
+
+def test_reference_engine_small_tori_bit_exact():
+    rows = golden("trials_small.json")["trials"]
+    groups = {}
+    for r in rows:
+        groups.setdefault((r["rows"], r["cols"], r["torus_seed"]), []).append(r)
+    for (R, C, s), rs in groups.items():
+        _check_rows(generate_torus(TorusSpec(R, C, s)), rs, lambda k: k)
+
+
+def test_reference_engine_random_graphs_bit_exact():
+    for g in golden("graphs_small.json")["graphs"]:
+        inst = ProblemInstance.from_edges(g["n"], [tuple(e) for e in g["edges"]])
+        for r in g["runs"]:
+            cfg = default_config(r["kind"], r["sweeps"], r["seed"])
+            b = run_trials(inst, cfg, [r["seed"]])
+            assert int(b.best_cut[0]) == r["best_cut"]
+            assert int(b.sweeps_executed[0]) == r["sweeps_executed"]
+            assert b.hex(0) == r["hex"]
+
+
+@pytest.mark.parametrize("kind", [ANNEALING, GREEDY])
+def test_reference_engine_config1_bit_exact(kind):
+    """BASELINE config 1 (50x100, 1000 sweeps) against the reference's own run."""
+    c1 = golden("c1_full.json")
+    inst = generate_torus(TorusSpec(50, 100, 1))
+    rows = c1["runs"][kind]["trials"]
+    if kind == ANNEALING:
+        rows = rows[:16]
+    cfg = default_config(kind, c1["sweeps"], 0)
+    b = run_trials(inst, cfg, [r["seed"] for r in rows])
+    for i, r in enumerate(rows):
+        assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+            r["best_cut"], r["sweeps_executed"], r["hex"]), r["index"]
+
+
+CHECKER_TORI = [(4, 4, 1), (4, 6, 3), (6, 6, 11), (8, 8, 42), (10, 12, 5), (16, 66, 2),
+                (4, 130, 7), (50, 100, 1), (100, 100, 1), (20, 64, 9)]
+
+
+@pytest.mark.parametrize("R,C,s", CHECKER_TORI)
+def test_checkerboard_engine_matches_oracle(oracle, R, C, s):
+    inst = generate_torus(TorusSpec(R, C, s))
+    w = inst.torus_weights
+    n = R * C
+    sweeps = 40 if n <= 1000 else 12
+    seeds = mix_seeds(MASTER, range(6))
+    for cfg in (default_config(ANNEALING_CHECKERBOARD, sweeps, 0),
+                SolverConfig(ANNEALING_CHECKERBOARD, sweeps, 0, 2.0, 0.1),
+                default_config(GREEDY_CHECKERBOARD, 200, 0)):
+        b = run_trials(inst, cfg, seeds)
+        bc, bs, se = oracle.run_trials_checker(R, C, w, cfg.kind, cfg.sweeps, seeds,
+                                               cfg.temp_start, cfg.temp_end)
+        for i in range(len(seeds)):
+            assert int(b.best_cut[i]) == bc[i], (cfg.kind, i)
+            assert int(b.sweeps_executed[i]) == se[i], (cfg.kind, i)
+            assert b.hex(i) == oracle.encode_hex(bs[i]), (cfg.kind, i)
+
+
+def test_checkerboard_batch_invariance():
+    inst = generate_torus(TorusSpec(50, 100, 1))
+    cfg = default_config(ANNEALING_CHECKERBOARD, 30, 0)
+    seeds = mix_seeds(MASTER, range(300))
+    full = run_trials(inst, cfg, seeds)
+    part = run_trials(inst, cfg, seeds[137:140])
+    assert np.array_equal(full.best_cut[137:140], part.best_cut)
+    assert np.array_equal(full.bits[137:140], part.bits)
+
+
+def test_checkerboard_best_bits_evaluate_to_best_cut():
+    inst = generate_torus(TorusSpec(100, 100, 1))
+    cfg = default_config(ANNEALING_CHECKERBOARD, 200, 0)
+    b = run_trials(inst, cfg, mix_seeds(MASTER, range(64)))
+    cut, en = cut_energy_batch(inst, b.bits)
+    assert np.array_equal(cut.cpu().numpy(), b.best_cut)
+    assert np.array_equal(en.cpu().numpy(), inst.total_weight() - 2 * b.best_cut)
+
+
+def test_checkerboard_rejects_odd_torus():
+    inst = generate_torus(TorusSpec(5, 6, 1))
+    with pytest.raises(ValueError):
+        run_trials(inst, default_config(ANNEALING_CHECKERBOARD, 5, 0), [1])
+
+
+def test_mix_seed_kat():
+    assert [mix_seed(1234567, i) for i in range(3)] == [
+        6457827717110365317, 3203168211198807973, 9817491932198370423]
