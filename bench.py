@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark of the sweep hot path (BASELINE.json metric: spin-updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c1|c2|c3|c4] [--kind KIND]
+
+One *step* = one batched campaign over this rank's trials: T trials x S sweeps
+of simulated annealing (default schedule 3.0 -> 0.05, solvers.py:31-32) on the
+seeded +-1 torus of the chosen BASELINE config, seeds mix_seed(20250814, i)
+(campaign.py:39-53), followed by the best-cut/bitstring reduction (NCCL when
+N > 1).  Default config c2 (BASELINE configs[1]: 100x100, 1024 trials x 10000
+sweeps), default kind the checkerboard (Philox) SA engine.  Weak scaling: every
+rank runs the full per-GPU trial count on its own trial indices.
+
+value = trials x sweeps x n x N x K / (max over ranks of the summed CUDA-event
+step times).  e2e = the same metric through the C ABI host-buffer entry
+(gsb_torus_sweep_host: H2D of weights/seeds/table and D2H of every result
+inside the timed region).  cpu_baseline / --impl reference = the reference's
+algorithm (oracle/ C port of solvers.run_trial, numpy-PCG64 stream,
+random-permutation sweeps) on all host cores, bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (rows, cols, trials per GPU, sweeps)  -- BASELINE.json configs[0..3]
+    "c1": (50, 100, 100, 1000),
+    "c2": (100, 100, 1024, 10_000),
+    "c3": (100, 140, 4096, 20_000),
+    "c4": (100, 200, 8192, 50_000),
+}
+MASTER = 20250814
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--kind", default="simulated_annealing_checkerboard")
+    ap.add_argument("--trials", type=int, default=None, help="override trials per GPU")
+    ap.add_argument("--sweeps", type=int, default=None, help="override sweeps")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = Path("/tmp") / f"gsb_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        try:
+            self.path.unlink()
+        except OSError:
+            pass
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "samples": len(sms), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- CPU baseline
+def cpu_port_rate(rows, cols, sweeps, seconds_target, threads=None):
+    """Reference algorithm (oracle C port of solvers.run_trial) on host cores.
+
+    Bounded sample: `threads` trials x the FULL sweep schedule when that fits
+    the time target, otherwise a prefix of the sweeps is timed (rate only).
+    """
+    from oracle import oracle as O
+
+    O.build()
+    threads = threads or os.cpu_count()
+    n = rows * cols
+    w = O.torus_weights(rows, cols, 1)
+    eu, ev, ew = O.torus_edges(rows, cols, w)
+    # calibrate on one short trial
+    t0 = time.perf_counter()
+    O.run_trials_ref(n, eu, ev, ew, "simulated_annealing", 20, [O.mix_seed(MASTER, 0)], 3.0, 0.05,
+                     spins=False, nthreads=1)
+    per_upd = (time.perf_counter() - t0) / (20 * n)
+    s_budget = max(10, min(sweeps, int(seconds_target / max(per_upd * n, 1e-12))))
+    seeds = [O.mix_seed(MASTER, i) for i in range(threads)]
+    t0 = time.perf_counter()
+    _, _, se = O.run_trials_ref(n, eu, ev, ew, "simulated_annealing", s_budget, seeds, 3.0, 0.05,
+                                spins=False, nthreads=threads)
+    dt = time.perf_counter() - t0
+    upd = int(se.sum()) * n
+    sample = (f"{threads} trials x {s_budget} sweeps of reference SA (PCG64 + permutation, "
+              f"schedule 3.0->0.05 over {s_budget} sweeps) on torus {rows}x{cols}:1, "
+              f"{threads} host threads")
+    return upd / dt, threads, sample, dt
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    rows, cols, T, S = CONFIGS[a.config]
+    S = a.sweeps or S
+    n = rows * cols
+    rates = []
+    for i in range(a.warmup + a.steps):
+        rate, cores, sample, dt = cpu_port_rate(rows, cols, S, max(a.cpu_seconds / 2, 4.0))
+        if i >= a.warmup:
+            rates.append(rate)
+    v = statistics.median(rates)
+    line = {
+        "impl": "reference",
+        "metric": "spin-updates/sec (trials x sweeps x n / s)",
+        "value": v, "unit": "spin-updates/s", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{a.config}: torus {rows}x{cols} seed 1, SA 3.0->0.05, "
+                               f"master seed {MASTER}", "trials_per_gpu": T, "sweeps": S, "n": n},
+        "cpu_baseline": {"value": v, "unit": "spin-updates/s", "cores": cores, "kind": "port",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": v, "unit": "spin-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "ms_per_step": None,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference_arm(a)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_18508_b200 import TorusSpec, _lib, generate_torus
+    from paper_2505_18508_b200.campaign import mix_seeds
+    from paper_2505_18508_b200.solvers import SolverConfig, default_config, schedule_table
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    rows, cols, T, S = CONFIGS[a.config]
+    T = a.trials or T
+    S = a.sweeps or S
+    n = rows * cols
+    cfg = default_config(a.kind, S, 0)
+    kind_code = _lib.GSB_ANNEALING if cfg.annealing else _lib.GSB_GREEDY
+    L = _lib.lib()
+    inst = generate_torus(TorusSpec(rows, cols, 1))
+    w = inst.device_weights(dev)
+    first = rank * T
+    seeds_np = mix_seeds(MASTER, range(first, first + T))
+    seeds = torch.from_numpy(seeds_np.view(np.int64).copy()).to(dev)
+    tab = schedule_table(cfg, 4)
+    tab_d = torch.from_numpy(tab.view(np.int64)).to(dev) if tab is not None else None
+    ts = _lib.torus_struct(rows, cols, w.data_ptr())
+    wsb = L.gsb_torus_workspace_bytes(ts, cfg.engine, S, T)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    best = torch.empty(T, dtype=torch.int64, device=dev)
+    sweeps_d = torch.empty(T, dtype=torch.int32, device=dev)
+    nbytes = (n + 7) // 8
+    bits = torch.empty((T, nbytes), dtype=torch.uint8, device=dev)
+    keys = torch.empty(T, dtype=torch.int64, device=dev)
+    win_bits = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    launches_per_step = 3  # checker masks + sweep kernel + best-key kernel (ours)
+
+    def sweep_launch():
+        _lib.check(L.gsb_torus_sweep(ts, cfg.engine, kind_code, S,
+                                     tab_d.data_ptr() if tab_d is not None else None,
+                                     seeds.data_ptr(), T, best.data_ptr(), sweeps_d.data_ptr(),
+                                     bits.data_ptr(), ws.data_ptr(), wsb, sp))
+
+    def reduce_best():
+        _lib.check(L.gsb_best_key(best.data_ptr(), T, first, keys.data_ptr(), sp))
+        kmax, arg = torch.max(keys, dim=0)
+        gkey = kmax.clone()
+        if world > 1:
+            dist.all_reduce(gkey, op=dist.ReduceOp.MAX)
+        # owner of the global winner broadcasts its bitstring
+        gk = int(gkey.item())
+        win_idx = 0xFFFFFFFF - (gk & 0xFFFFFFFF)
+        owner = win_idx // T
+        if owner == rank:
+            win_bits.copy_(bits[win_idx - first])
+        if world > 1:
+            dist.broadcast(win_bits, src=int(owner))
+        return gk >> 32, win_idx
+
+    def step(ev0=None, ev1=None, kev=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        sweep_launch()
+        if kev is not None:
+            kev.record(stream)
+        res = reduce_best()
+        if ev1 is not None:
+            ev1.record(stream)
+        return res
+
+    # warm-up (also validates the integrity guard once)
+    for _ in range(max(a.warmup, 0)):
+        step()
+    _lib.check(L.gsb_workspace_status(ws.data_ptr(), sp))
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    wall0 = time.perf_counter()
+    step_ms, kern_ms = [], []
+    for _ in range(a.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the event window)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ek = torch.cuda.Event(enable_timing=True)
+        best_cut_global, win_idx = step(e0, e1, ek)
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        kern_ms.append(e0.elapsed_time(ek))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clk = clocks.stop()
+    _lib.check(L.gsb_workspace_status(ws.data_ptr(), sp))
+
+    tot_ms = sum(step_ms)
+    tot_kern = sum(kern_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms, tot_kern], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, tot_kern = float(t[0]), float(t[1])
+    upd_per_step_rank = T * S * n
+    value = upd_per_step_rank * world * a.steps / (tot_ms / 1e3)
+    kernel_rate = upd_per_step_rank / (tot_kern / a.steps / 1e3)  # per GPU
+
+    # ---- e2e through the C ABI host-buffer entry (pinned host memory)
+    e2e = None
+    if not a.no_e2e:
+        w_h = torch.from_numpy(inst.torus_weights.copy()).pin_memory()
+        s_h = torch.from_numpy(seeds_np.view(np.int64).copy()).pin_memory()
+        bc_h = torch.empty(T, dtype=torch.int64).pin_memory()
+        se_h = torch.empty(T, dtype=torch.int32).pin_memory()
+        bits_h = torch.empty((T, nbytes), dtype=torch.uint8).pin_memory()
+        t0c = cfg.temp_start or 0.0
+        t1c = cfg.temp_end or 0.0
+
+        def host_call():
+            _lib.check(L.gsb_torus_sweep_host(rows, cols, w_h.data_ptr(), cfg.engine, kind_code, S,
+                                              t0c, t1c, s_h.data_ptr(), T, bc_h.data_ptr(),
+                                              se_h.data_ptr(), bits_h.data_ptr(), sp))
+
+        host_call()
+        if world > 1:
+            dist.barrier()
+        e2e_s = []
+        for _ in range(a.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            host_call()
+            e2e_s.append(time.perf_counter() - t0)
+        tot_e2e = sum(e2e_s)
+        if world > 1:
+            t = torch.tensor([tot_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_e2e = float(t[0])
+        assert np.array_equal(bc_h.numpy(), best.cpu().numpy()), "e2e results differ"
+        h2d = 2 * n + 8 * T + (tab.nbytes if tab is not None else 0)
+        d2h = 8 * T + 4 * T + T * nbytes
+        e2e = {"value": upd_per_step_rank * world * a.steps / tot_e2e, "unit": "spin-updates/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": tot_e2e / a.steps * 1e3,
+               "api": "gsb_torus_sweep_host (include/gsb.h)"}
+
+    # ---- roofline of the dominant kernel (the sweep kernel)
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    smem_peak = nsm * 128 * f_max  # B/s, 128 B/clk/SM crossbar
+    b_alg = 1.25  # bit-packed 5-point stencil: 10 bits per update
+    achieved_bw = kernel_rate * b_alg
+    roofline = {
+        "bound": "smem", "unit": "GB/s",
+        "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9,
+        "frac": achieved_bw / smem_peak, "traffic": None,
+        "kernel": "gsb::checker_sweep_kernel",
+        "algorithmic_bytes_per_update": b_alg,
+        "updates_per_launch": upd_per_step_rank,
+        "launch_ms": tot_kern / a.steps,
+        "peak_basis": f"{nsm} SMs x 128 B/clk x sm_max {f_max / 1e6:.0f} MHz (computed, "
+                      "no measured SMEM peak in MEASURED_PEAKS.json)",
+        "note": "kernel is integer-issue bound (Philox4x32-10 + bit-sliced stencil); "
+                "see DESIGN.md and profiles/ for the int-issue figures",
+    }
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        rate, cores, sample, dt = cpu_port_rate(rows, cols, S, a.cpu_seconds)
+        cpu = {"value": rate, "unit": "spin-updates/s", "cores": cores, "kind": "port",
+               "sample": sample, "seconds": round(dt, 2), "cpu": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": "spin-updates/sec (trials x sweeps x n / s)",
+            "value": value, "unit": "spin-updates/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": tot_ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded +-1 torus, generate_torus weights)",
+            "config": {
+                "workload": f"{a.config}: torus {rows}x{cols} seed 1, {a.kind}, "
+                            f"{T} trials/GPU x {S} sweeps, SA 3.0->0.05, master seed {MASTER}",
+                "trials_per_gpu": T, "sweeps": S, "n": n, "kind": a.kind,
+                "parallelism": f"trials sharded over {world} GPU(s), NCCL best-cut reduction",
+                "l2": "flushed between timed steps (2x126 MiB memset outside the event window)",
+            },
+            "per_gpu_value": value / world,
+            "best_cut": int(best_cut_global), "best_trial": int(win_idx),
+            "wall_s_timed_region": wall,
+            "gpu_launches": launches_per_step * a.steps,
+            "clocks": clk,
+            "roofline": roofline,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -107,6 +107,13 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
                     int64_t *best_cut_dev, int32_t *sweeps_executed_dev, uint8_t *best_bits_dev,
                     void *workspace_dev, size_t workspace_bytes, void *stream);
 
+/* The sweep calls are asynchronous on `stream`.  The integrity guard of
+ * solvers.py:132-133 (best_cut == cut of the best bitstring, recomputed on
+ * the device) is recorded in the workspace; gsb_workspace_status synchronises
+ * `stream` and returns GSB_OK or GSB_EINTEGRITY for the last sweep call that
+ * used this workspace. */
+int gsb_workspace_status(const void *workspace_dev, void *stream);
+
 /* reference engine on a general graph (any integer weights, dmax = max_i sum_j |w_ij|) */
 size_t gsb_graph_workspace_bytes(const gsb_graph *g, int32_t sweeps, int32_t T);
 int gsb_graph_sweep(const gsb_graph *g, int kind, int32_t sweeps, const uint64_t *table_dev,

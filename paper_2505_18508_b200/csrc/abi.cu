@@ -180,8 +180,12 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   } else {
     return set_error(GSB_EINVAL, "unknown engine");
   }
-  if (rc) return rc;
-  return finish_check(err, stream);
+  return rc;
+}
+
+int gsb_workspace_status(const void *ws, void *stream) {
+  if (!ws) return set_error(GSB_EINVAL, "null workspace");
+  return finish_check((int *)ws, (cudaStream_t)stream);
 }
 
 size_t gsb_graph_workspace_bytes(const gsb_graph *g, int32_t sweeps, int32_t T) {
@@ -206,11 +210,9 @@ int gsb_graph_sweep(const gsb_graph *g, int kind, int32_t sweeps, const uint64_t
   int *err = (int *)ws;
   if (cudaMemsetAsync(err, 0, sizeof(int), stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
-  int rc = ref_run_graph(g, kind, sweeps, table, dmax < 1 ? 1 : dmax, seeds, T, best_cut,
-                         sweeps_exec, best_bits, (char *)ws + err_bytes(),
-                         ws_bytes - err_bytes(), err, stream);
-  if (rc) return rc;
-  return finish_check(err, stream);
+  return ref_run_graph(g, kind, sweeps, table, dmax < 1 ? 1 : dmax, seeds, T, best_cut,
+                       sweeps_exec, best_bits, (char *)ws + err_bytes(), ws_bytes - err_bytes(),
+                       err, stream);
 }
 
 int gsb_torus_sweep_host(int32_t rows, int32_t cols, const int8_t *w_host, int engine, int kind,
@@ -261,6 +263,8 @@ int gsb_torus_sweep_host(int32_t rows, int32_t cols, const int8_t *w_host, int e
   GSB_TRY(cudaMemcpyAsync(seeds, seeds_host, sizeof(uint64_t) * T, cudaMemcpyHostToDevice, stream));
   inst.w_dev = w;
   rc = gsb_torus_sweep(&inst, engine, kind, sweeps, tab, seeds, T, bc, se, bits, ws, wsb, stream);
+  if (rc) goto done;
+  rc = finish_check((int *)ws, stream);
   if (rc) goto done;
   GSB_TRY(cudaMemcpyAsync(best_cut_host, bc, sizeof(int64_t) * T, cudaMemcpyDeviceToHost, stream));
   GSB_TRY(cudaMemcpyAsync(sweeps_exec_host, se, sizeof(int32_t) * T, cudaMemcpyDeviceToHost, stream));

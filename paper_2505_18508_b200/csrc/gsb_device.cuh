@@ -18,9 +18,8 @@ struct P4 {
 };
 
 __device__ __forceinline__ void mulwide(uint32_t a, uint32_t b, uint32_t &hi, uint32_t &lo) {
-  uint64_t p = (uint64_t)a * (uint64_t)b;  // IMAD.WIDE.U32
-  hi = (uint32_t)(p >> 32);
-  lo = (uint32_t)p;
+  hi = __umulhi(a, b);
+  lo = a * b;
 }
 
 __device__ __forceinline__ P4 philox10(P4 c, uint32_t k0, uint32_t k1) {

@@ -154,12 +154,14 @@ def _graph_dmax(instance: ProblemInstance) -> int:
 
 
 def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, device=None,
-                      stream=None):
+                      stream=None, check: bool = True):
     """Batched trials with device-resident outputs (torch tensors).
 
     ``seeds`` is a uint64-valued sequence or an int64 CUDA tensor holding the
     seed bit patterns.  Returns (best_cut int64 [T], sweeps_executed int32 [T],
-    bits uint8 [T, ceil(n/8)]) on ``device``.
+    bits uint8 [T, ceil(n/8)]) on ``device``.  With ``check`` (default) the
+    call synchronises and raises RuntimeError if the device integrity guard
+    (solvers.py:132-133) fired; without it the launch stays asynchronous.
     """
     torch = _lib.require_cuda()
     dev = torch.device(device if device is not None else "cuda")
@@ -195,6 +197,8 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
                                          seeds_d.data_ptr(), T, best.data_ptr(),
                                          sweeps.data_ptr(), bits.data_ptr(), ws.data_ptr(), wsb,
                                          sp))
+            if check:
+                _lib.check(L.gsb_workspace_status(ws.data_ptr(), sp))
         else:
             if config.engine != _lib.ENGINE_REFERENCE:
                 raise ValueError("checkerboard kinds need a torus instance")
@@ -210,6 +214,8 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
                                          seeds_d.data_ptr(), T, best.data_ptr(),
                                          sweeps.data_ptr(), bits.data_ptr(), ws.data_ptr(), wsb,
                                          sp))
+            if check:
+                _lib.check(L.gsb_workspace_status(ws.data_ptr(), sp))
     return best, sweeps, bits
 
 
