@@ -125,9 +125,7 @@ size_t gsb_torus_workspace_bytes(const gsb_torus *inst, int engine, int32_t swee
   int n = inst->rows * inst->cols;
   size_t b = err_bytes();
   if (engine == GSB_ENGINE_CHECKERBOARD) {
-    int WPR, nw;
-    checker_words(inst->rows, inst->cols, &WPR, &nw);
-    b += align_up((size_t)2 * nw * 8 * 4, 256);
+    b += checker_workspace_bytes(inst->rows, inst->cols);
   } else {
     b += ref_workspace_bytes(n, 0, T);
   }
@@ -173,7 +171,7 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     if (!checker_fits(inst->rows, inst->cols))
       return set_error(GSB_EUNSUPPORTED, "torus too large for the shared-memory engine");
     rc = checker_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
-                     sweeps_exec, best_bits, (uint32_t *)rest, err, stream);
+                     sweeps_exec, best_bits, rest, err, stream);
   } else if (engine == GSB_ENGINE_REFERENCE) {
     rc = ref_run_torus(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, 4, seeds, T,
                        best_cut, sweeps_exec, best_bits, rest, rest_bytes, err, stream);

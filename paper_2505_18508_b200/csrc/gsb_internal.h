@@ -15,9 +15,10 @@ int num_sms();
 // checkerboard engine (checker.cu)
 int checker_words(int rows, int cols, int *WPR, int *nw);
 bool checker_fits(int rows, int cols);
+size_t checker_workspace_bytes(int rows, int cols);
 int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                 const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
-                int32_t *sweeps_exec, uint8_t *best_bits, uint32_t *masks_ws, int *err_ws,
+                int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                 cudaStream_t stream);
 
 // reference-exact engine (refexact.cu)
