@@ -362,27 +362,35 @@ int gso_run_trial_ref(int32_t n, int64_t m, const int32_t *eu, const int32_t *ev
 /* ------------------------------------------------------------------ */
 /* checkerboard (Philox) trial -- DESIGN.md "Checkerboard contract"     */
 /* ------------------------------------------------------------------ */
-/* uniform of site (r, k) of colour p at sweep t: 32 bit planes, plane j is
-   word (j & 3) of Philox(key, (wi, t, 8p + (j >> 2), 1)), wi = r*WPR + (k>>5);
-   bit (k & 31) of plane j is bit (31 - j) of the uniform. */
+/* Uniform of site (r, k) of colour p at sweep t (contract v2):
+ *   wi = r*WPR + (k>>5), b = k & 31,
+ *   planes j = 0..7: word (j & 3) of Philox(key, (wi, t, 2p + (j >> 2), 1));
+ *   u bits 31..24 = bit b of planes 0..7 (plane 0 = MSB);
+ *   u bits 23..0  = (word (b & 3) of Philox(key, (wi, t, 4 + 8p + (b >> 2), 1))) >> 8. */
 typedef struct {
     uint32_t key[2];
     int32_t t, p, wi;
-    uint32_t planes[32];
+    uint32_t planes[8];
+    uint32_t tail[32];
 } plane_cache;
 
 static uint32_t checker_uniform(plane_cache *pc, int32_t t, int32_t p, int32_t wi, int bit) {
     if (pc->t != t || pc->p != p || pc->wi != wi) {
-        for (int g = 0; g < 8; g++) {
-            uint32_t ctr[4] = {(uint32_t)wi, (uint32_t)t, (uint32_t)(8 * p + g), 1u};
+        for (int g = 0; g < 2; g++) {
+            uint32_t ctr[4] = {(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p + g), 1u};
             gso_philox4x32_10(ctr, pc->key, &pc->planes[4 * g]);
+        }
+        for (int q = 0; q < 8; q++) {
+            uint32_t ctr[4] = {(uint32_t)wi, (uint32_t)t, (uint32_t)(4 + 8 * p + q), 1u};
+            gso_philox4x32_10(ctr, pc->key, &pc->tail[4 * q]);
         }
         pc->t = t;
         pc->p = p;
         pc->wi = wi;
     }
     uint32_t u = 0;
-    for (int j = 0; j < 32; j++) u |= ((pc->planes[j] >> bit) & 1u) << (31 - j);
+    for (int j = 0; j < 8; j++) u |= ((pc->planes[j] >> bit) & 1u) << (31 - j);
+    u |= pc->tail[bit] >> 8;
     return u;
 }
 

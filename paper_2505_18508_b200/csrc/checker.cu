@@ -19,8 +19,9 @@
 // Per word and half-sweep: 4 positive-term planes P_j = ~(S^N_j^NEG_j),
 // bit-sliced counts -> Delta classes, then for the Delta<0 sites an MSB-first
 // bit-sliced comparison of the 32-bit uniform with K = ceil(exp(Delta/T)*2^32):
-// Philox planes 0-7 are drawn unconditionally (two calls), later planes only
-// while a site of the word is still undecided.
+// uniform bits 31..24 are 8 Philox planes (two calls per word, unconditional);
+// sites still undecided after them take bits 23..0 from a per-site Philox word
+// (contract v2), drawn for the whole warp in one cooperative round.
 //
 // Best-so-far (solvers.py:125-127) per half-sweep: the running cut in visit
 // order is cur + prefix sum of the accepted Deltas; a block reduction gives the
@@ -36,31 +37,37 @@
 
 namespace gsb {
 
-// masks: [2][nw] uint4 {NS, NSH, NU, ND} (bit = weight -1) and valid[2][nw]
+// Setup tables (shared by every trial on this instance):
+//   masks[2][nw] uint4 {NS, NSH, NU, ND}: bit = coupling weight is -1, for the
+//     same-k / shifted / up / down neighbour of each site of word (p, wi);
+//   geo[nw] uint4 {up | dn<<16, cidx0 | cidx1<<16, cinfo0 | cinfo1<<16, valid}:
+//     neighbour word indices, carry word + bit info of the shifted neighbour
+//     per colour, valid-bit mask (same for both colours).
 __global__ void checker_masks_kernel(int rows, int cols, int WPR, const int8_t *__restrict__ w,
-                                     uint4 *__restrict__ masks, uint32_t *__restrict__ valid) {
+                                     uint4 *__restrict__ masks, uint4 *__restrict__ geo) {
   const int H = cols >> 1;
   const int nw = rows * WPR;
+  const int lb = (H - 1) & 31;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nw;
        idx += gridDim.x * blockDim.x) {
-    int p = idx / nw, wi = idx % nw;
-    int r = wi / WPR, ww = wi % WPR;
-    int e = (r + p) & 1;
+    const int p = idx / nw, wi = idx % nw;
+    const int r = wi / WPR, ww = wi % WPR;
+    const int e = (r + p) & 1;
     uint32_t ns = 0, nsh = 0, nu = 0, nd = 0, v = 0;
     for (int b = 0; b < 32; b++) {
-      int k = ww * 32 + b;
+      const int k = ww * 32 + b;
       if (k >= H) break;
-      int c = 2 * k + e;
-      int x = r * cols + c;
-      int cl = (c + cols - 1) % cols;
-      int ru = (r + rows - 1) % rows;
-      int8_t w_right = w[2 * x], w_down = w[2 * x + 1];
-      int8_t w_left = w[2 * (r * cols + cl)];
-      int8_t w_up = w[2 * (ru * cols + c) + 1];
+      const int c = 2 * k + e;
+      const int x = r * cols + c;
+      const int cl = (c + cols - 1) % cols;
+      const int ru = (r + rows - 1) % rows;
+      const int8_t w_right = w[2 * x], w_down = w[2 * x + 1];
+      const int8_t w_left = w[2 * (r * cols + cl)];
+      const int8_t w_up = w[2 * (ru * cols + c) + 1];
       // e==0: same-k other-colour word is the right neighbour, shifted is left
       // e==1: same-k is the left neighbour, shifted is right
-      int8_t wsame = e == 0 ? w_right : w_left;
-      int8_t wsh = e == 0 ? w_left : w_right;
+      const int8_t wsame = e == 0 ? w_right : w_left;
+      const int8_t wsh = e == 0 ? w_left : w_right;
       v |= 1u << b;
       if (wsame < 0) ns |= 1u << b;
       if (wsh < 0) nsh |= 1u << b;
@@ -68,14 +75,29 @@ __global__ void checker_masks_kernel(int rows, int cols, int WPR, const int8_t *
       if (w_down < 0) nd |= 1u << b;
     }
     masks[idx] = make_uint4(ns, nsh, nu, nd);
-    valid[idx] = v;
+    if (p == 0) {
+      uint32_t cidx[2], cinfo[2];
+      for (int q = 0; q < 2; q++) {
+        if (((r + q) & 1) == 0) {  // k-1 neighbour: carry from the previous word (or row end)
+          cidx[q] = ww > 0 ? wi - 1 : r * WPR + WPR - 1;
+          cinfo[q] = (uint32_t)(ww > 0 ? 31 : lb);
+        } else {  // k+1 neighbour: carry from the next word (or row start)
+          cidx[q] = ww < WPR - 1 ? wi + 1 : r * WPR;
+          cinfo[q] = ((uint32_t)(ww < WPR - 1 ? 31 : lb) << 5) | (1u << 10);
+        }
+      }
+      const uint32_t up = (r == 0 ? rows - 1 : r - 1) * WPR + ww;
+      const uint32_t dn = (r == rows - 1 ? 0 : r + 1) * WPR + ww;
+      geo[wi] = make_uint4(up | (dn << 16), cidx[0] | (cidx[1] << 16), cinfo[0] | (cinfo[1] << 16),
+                           v);
+    }
   }
 }
 
 struct CheckerArgs {
   int rows, cols, H, WPR, nw, lb;
   const uint4 *masks;
-  const uint32_t *valid;
+  const uint4 *geo;
   const uint64_t *table;  // [S][4]
   int sweeps;
   const uint64_t *seeds;
@@ -87,15 +109,8 @@ struct CheckerArgs {
   int *err;
 };
 
-// per-thread geometry of one owned word (both colours share up/dn rows)
-struct WordGeo {
-  int up, dn;         // word index of the row above / below (same ww)
-  int cidx[2];        // carry word for colour p (shifted neighbour)
-  uint32_t cinfo[2];  // bits 0-4: source bit, 5-9: destination bit, 10: direction (1 = k+1)
-};
-
 __device__ __forceinline__ uint32_t shifted_nb(const uint32_t *__restrict__ o, uint32_t same,
-                                               int cidx, uint32_t cinfo) {
+                                               uint32_t cidx, uint32_t cinfo) {
   const uint32_t src = cinfo & 31u, dst = (cinfo >> 5) & 31u;
   const uint32_t carry = ((o[cidx] >> src) & 1u) << dst;
   return ((cinfo >> 10) & 1u) ? ((same >> 1) | carry) : ((same << 1) | carry);
@@ -117,65 +132,82 @@ __device__ __forceinline__ int word_cut(uint32_t s, uint32_t same, uint32_t sh, 
   return c;
 }
 
-// MSB-first bit-sliced compare step for the 4 planes of Philox group g
-__device__ __forceinline__ void cmp_planes(P4 r, int g, uint32_t K2, uint32_t K4, uint32_t e2,
-                                           uint32_t e4, uint32_t &eq, uint32_t &lt) {
-  const uint32_t pl[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const int bit = 31 - (4 * g + q);
-    const uint32_t m2 = (uint32_t)((int32_t)(K2 << (31 - bit)) >> 31);
-    const uint32_t m4 = (uint32_t)((int32_t)(K4 << (31 - bit)) >> 31);
-    const uint32_t tb = (e2 & m2) | (e4 & m4);
-    const uint32_t R = pl[q];
-    lt |= eq & ~R & tb;
-    eq &= ~(R ^ tb);
-  }
+// Delta classes of a word (bit-sliced counts of the 4 positive-term planes)
+struct Classes {
+  uint32_t ge2, k3, k4, km2, km4;
+};
+
+__device__ __forceinline__ Classes classes(uint32_t Sw, uint32_t same, uint32_t sh, uint32_t up,
+                                           uint32_t dn, uint4 m, uint32_t V) {
+  const uint32_t P0 = ~(Sw ^ same ^ m.x);
+  const uint32_t P1 = ~(Sw ^ sh ^ m.y);
+  const uint32_t P2 = ~(Sw ^ up ^ m.z);
+  const uint32_t P3 = ~(Sw ^ dn ^ m.w);
+  const uint32_t x01 = P0 ^ P1, c01 = P0 & P1, x23 = P2 ^ P3, c23 = P2 & P3;
+  const uint32_t ones = x01 ^ x23;
+  Classes c;
+  c.ge2 = (c01 | c23 | (x01 & x23)) & V;  // Delta >= 0
+  c.k4 = c01 & c23 & V;                    // Delta = +4
+  c.k3 = ((c01 | c23) & ones) & V;         // Delta = +2
+  const uint32_t any = P0 | P1 | P2 | P3;
+  c.km2 = any & ~c.ge2 & V;  // Delta = -2
+  c.km4 = ~any & V;          // Delta = -4
+  return c;
+}
+
+// MSB-first bit-sliced compare step for one plane.  c2 = class -2 sites
+// (threshold K2), other pending sites use K4; ma/mb = all-ones iff the
+// plane's bit of K2/K4 is set (per sweep, uniform).  4 LOP3 per plane.
+__device__ __forceinline__ void cmp_plane(uint32_t R, uint32_t c2, uint32_t ma, uint32_t mb,
+                                          uint32_t &eq, uint32_t &lt) {
+  const uint32_t tb = (c2 & ma) | (~c2 & mb);
+  lt |= eq & ~R & tb;
+  eq &= ~(R ^ tb);
+}
+
+// 8-bit mask of the non-zero nibbles of x (bit g <-> nibble g)
+__device__ __forceinline__ uint32_t nibmask8(uint32_t x) {
+  x |= x >> 1;
+  x |= x >> 2;
+  x &= 0x11111111u;
+  x = (x | (x >> 3)) & 0x03030303u;
+  x = (x | (x >> 6)) & 0x000F000Fu;
+  x = (x | (x >> 12)) & 0xFFu;
+  return x;
 }
 
 template <int NT, int WPT, bool SA>
 __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
   constexpr int NWARP = NT / 32;
+  static_assert(WPT <= 8, "tail item index packs 8 words x 8 groups");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = a.nw;
-  uint4 *msk = (uint4 *)smem_raw;             // [2][nw]
-  uint32_t *st = (uint32_t *)(msk + 2 * nw);  // [2][nw] neighbour copy
-  uint32_t *bst = st + 2 * nw;                // [2][nw] best snapshot
-  int *red = (int *)(bst + 2 * nw);           // [2 buffers][2][NWARP]
-  int *red2 = red + 4 * NWARP;                // [2][NWARP] misc
-  int *scan = red2 + 2 * NWARP;               // [WPT][NWARP]
+  uint4 *msk = (uint4 *)smem_raw;                 // [2][nw]
+  uint4 *geo = msk + 2 * nw;                      // [nw]
+  uint32_t *st = (uint32_t *)(geo + nw);          // [2][nw] neighbour copy
+  uint32_t *bst = st + 2 * nw;                    // [2][nw] best snapshot
+  uint32_t *tx = bst + 2 * nw;                    // [NWARP][3][WPT][32] tail exchange
+  uint32_t *tq = tx + NWARP * 3 * WPT * 32;       // [NWARP][32] tail queue
+  int *red = (int *)(tq + NWARP * 32);            // [2 buffers][2][NWARP]
+  int *red2 = red + 4 * NWARP;                    // [2][NWARP]
+  int *scan = red2 + 2 * NWARP;                   // [WPT][NWARP]
   long long *kred = (long long *)(scan + ((WPT * NWARP + 1) & ~1));  // [NWARP]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  uint32_t *teq = tx + warp * 3 * WPT * 32;  // [WPT][32] pending masks
+  uint32_t *tc2 = teq + WPT * 32;            // [WPT][32] class -2 masks
+  uint32_t *tlt = tc2 + WPT * 32;            // [WPT][32] accepted-by-tail bits
+  uint32_t *myq = tq + warp * 32;
 
-  // ---- per-kernel setup: couplings to shared memory, per-thread geometry
   for (int i = tid; i < 2 * nw; i += NT) msk[i] = a.masks[i];
-  WordGeo geo[WPT];
-  uint32_t vmask[2][WPT];
+  for (int i = tid; i < nw; i += NT) geo[i] = a.geo[i];
+  for (int i = tid; i < NWARP * 3 * WPT * 32; i += NT) tx[i] = 0;
+  __syncthreads();
+
   bool own[WPT];
 #pragma unroll
-  for (int j = 0; j < WPT; j++) {
-    const int wi = j * NT + tid;
-    own[j] = wi < nw;
-    const int wic = own[j] ? wi : 0;
-    const int r = wic / a.WPR, ww = wic - r * a.WPR;
-    geo[j].up = (r == 0 ? a.rows - 1 : r - 1) * a.WPR + ww;
-    geo[j].dn = (r == a.rows - 1 ? 0 : r + 1) * a.WPR + ww;
-#pragma unroll
-    for (int p = 0; p < 2; p++) {
-      const int e = (r + p) & 1;
-      if (e == 0) {  // k-1 neighbour: carry from the previous word (or row end)
-        geo[j].cidx[p] = ww > 0 ? wic - 1 : r * a.WPR + a.WPR - 1;
-        geo[j].cinfo[p] = (uint32_t)(ww > 0 ? 31 : a.lb);
-      } else {  // k+1 neighbour: carry from the next word (or row start)
-        geo[j].cidx[p] = ww < a.WPR - 1 ? wic + 1 : r * a.WPR;
-        geo[j].cinfo[p] = ((uint32_t)(ww < a.WPR - 1 ? 31 : a.lb) << 5) | (1u << 10);
-      }
-      vmask[p][j] = own[j] ? a.valid[p * nw + wi] : 0u;
-    }
-  }
-  __syncthreads();
+  for (int j = 0; j < WPT; j++) own[j] = j * NT + tid < nw;
 
   for (int trial = blockIdx.x; trial < a.T; trial += gridDim.x) {
     const uint64_t seed = a.seeds[trial];
@@ -186,12 +218,13 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
 #pragma unroll
     for (int j = 0; j < WPT; j++) {
       const int wi = j * NT + tid;
+      S[0][j] = S[1][j] = 0;
+      if (own[j]) {
+        const uint32_t V = geo[wi].w;
 #pragma unroll
-      for (int p = 0; p < 2; p++) {
-        S[p][j] = 0;
-        if (own[j]) {
-          P4 o = philox10(P4{(uint32_t)wi, 0u, (uint32_t)p, 0u}, key0, key1);
-          S[p][j] = o.x & vmask[p][j];
+        for (int p = 0; p < 2; p++) {
+          const P4 o = philox10(P4{(uint32_t)wi, 0u, (uint32_t)p, 0u}, key0, key1);
+          S[p][j] = o.x & V;
           st[p * nw + wi] = S[p][j];
           bst[p * nw + wi] = S[p][j];
         }
@@ -205,10 +238,10 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
     for (int j = 0; j < WPT; j++) {
       if (own[j]) {
         const int wi = j * NT + tid;
+        const uint4 g = geo[wi];
         const uint32_t *o = st + nw;
-        const uint32_t same = S[1][j];
-        const uint32_t sh = shifted_nb(o, same, geo[j].cidx[0], geo[j].cinfo[0]);
-        c0 += word_cut(S[0][j], same, sh, o[geo[j].up], o[geo[j].dn], msk[wi], vmask[0][j]);
+        const uint32_t sh = shifted_nb(o, S[1][j], g.y & 0xFFFFu, g.z & 0xFFFFu);
+        c0 += word_cut(S[0][j], S[1][j], sh, o[g.x & 0xFFFFu], o[g.x >> 16], msk[wi], g.w);
       }
     }
     c0 = (int)__reduce_add_sync(0xffffffffu, (unsigned)c0);
@@ -231,137 +264,232 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
         K2 = (uint32_t)t2;
         K4 = (uint32_t)t4;
       }
-      bool sweep_flipped = false;
+      // per-sweep plane masks (bits 31..24 of K2 / K4)
+      uint32_t ma[8], mb[8];
 #pragma unroll
+      for (int q = 0; q < 8; q++) {
+        ma[q] = (uint32_t)((int32_t)(K2 << q) >> 31);
+        mb[q] = (uint32_t)((int32_t)(K4 << q) >> 31);
+      }
+      const uint32_t K2lo = K2 & 0xFFFFFFu, K4lo = K4 & 0xFFFFFFu;
+      bool sweep_flipped = false;
+#pragma unroll 1
       for (int p = 0; p < 2; p++, buf ^= 1) {
         const uint32_t *o = st + (p ^ 1) * nw;
-        uint32_t Am[WPT], Pos2[WPT], Pos4[WPT], Neg2[WPT], Neg4[WPT];
-        int dsum = 0, psum = 0;
+        uint32_t A[WPT], c2[WPT], eq[WPT], lt[WPT];
+        int wpos[WPT], wsum[WPT];
+        uint64_t itm = 0;
+        // ---- pass 1: classes and the unconditional planes 0-7
 #pragma unroll
         for (int j = 0; j < WPT; j++) {
           const int wi = j * NT + tid;
-          Am[j] = Pos2[j] = Pos4[j] = Neg2[j] = Neg4[j] = 0;
+          A[j] = c2[j] = eq[j] = lt[j] = 0;
+          wpos[j] = wsum[j] = 0;
           if (own[j]) {
+            const uint4 g = geo[wi];
             const uint4 m = msk[p * nw + wi];
-            const uint32_t V = vmask[p][j];
-            const uint32_t Sw = S[p][j];
             const uint32_t same = S[p ^ 1][j];
-            const uint32_t sh = shifted_nb(o, same, geo[j].cidx[p], geo[j].cinfo[p]);
-            const uint32_t up = o[geo[j].up], dn = o[geo[j].dn];
-            const uint32_t P0 = ~(Sw ^ same ^ m.x);
-            const uint32_t P1 = ~(Sw ^ sh ^ m.y);
-            const uint32_t P2 = ~(Sw ^ up ^ m.z);
-            const uint32_t P3 = ~(Sw ^ dn ^ m.w);
-            const uint32_t x01 = P0 ^ P1, c01 = P0 & P1, x23 = P2 ^ P3, c23 = P2 & P3;
-            const uint32_t ones = x01 ^ x23;
-            const uint32_t ge2 = c01 | c23 | (x01 & x23);  // Delta >= 0
-            const uint32_t k4 = c01 & c23 & V;             // Delta = +4
-            const uint32_t k3 = ((c01 | c23) & ones) & V;  // Delta = +2
-            const uint32_t any = P0 | P1 | P2 | P3;
-            const uint32_t km2 = any & ~ge2 & V;           // Delta = -2
-            const uint32_t km4 = ~any & V;                 // Delta = -4
-            uint32_t A;
+            const uint32_t sh = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
+                                           p ? (g.z >> 16) : (g.z & 0xFFFFu));
+            const Classes c = classes(S[p][j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m, g.w);
+            wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
             if (SA) {
-              A = ge2 & V;
-              if (all2) A |= km2;
-              if (all4) A |= km4;
-              const uint32_t e2 = (all2 || K2 == 0) ? 0u : km2;
-              const uint32_t e4 = (all4 || K4 == 0) ? 0u : km4;
-              uint32_t eq = e2 | e4, lt = 0;
-              const P4 r0 =
-                  philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(8 * p), 1u}, key0, key1);
-              const P4 r1 =
-                  philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(8 * p + 1), 1u}, key0, key1);
-              cmp_planes(r0, 0, K2, K4, e2, e4, eq, lt);
-              cmp_planes(r1, 1, K2, K4, e2, e4, eq, lt);
-#pragma unroll 1
-              for (int g = 2; g < 8 && eq; g++) {
-                const P4 r =
-                    philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(8 * p + g), 1u}, key0, key1);
-                cmp_planes(r, g, K2, K4, e2, e4, eq, lt);
+              uint32_t b = c.ge2;
+              int neg = 0;
+              if (all2) {
+                b |= c.km2;
+                neg += 2 * __popc(c.km2);
               }
-              A |= lt;
+              if (all4) {
+                b |= c.km4;
+                neg += 4 * __popc(c.km4);
+              }
+              A[j] = b;
+              wsum[j] = wpos[j] - neg;
+              const uint32_t e2 = (all2 || K2 == 0) ? 0u : c.km2;
+              const uint32_t e4 = (all4 || K4 == 0) ? 0u : c.km4;
+              c2[j] = e2;
+              uint32_t q = e2 | e4, l = 0;
+              const P4 r0 =
+                  philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p), 1u}, key0, key1);
+              const P4 r1 =
+                  philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p + 1), 1u}, key0, key1);
+              cmp_plane(r0.x, e2, ma[0], mb[0], q, l);
+              cmp_plane(r0.y, e2, ma[1], mb[1], q, l);
+              cmp_plane(r0.z, e2, ma[2], mb[2], q, l);
+              cmp_plane(r0.w, e2, ma[3], mb[3], q, l);
+              cmp_plane(r1.x, e2, ma[4], mb[4], q, l);
+              cmp_plane(r1.y, e2, ma[5], mb[5], q, l);
+              cmp_plane(r1.z, e2, ma[6], mb[6], q, l);
+              cmp_plane(r1.w, e2, ma[7], mb[7], q, l);
+              eq[j] = q;
+              lt[j] = l;
+              if (q) {
+                teq[j * 32 + lane] = q;
+                tc2[j * 32 + lane] = e2;
+                itm |= (uint64_t)nibmask8(q) << (8 * j);
+              }
             } else {
-              A = k4 | k3;
+              A[j] = c.k3 | c.k4;
+              wsum[j] = wpos[j];
             }
-            const uint32_t Sn = Sw ^ A;
-            S[p][j] = Sn;
-            st[p * nw + wi] = Sn;
-            Am[j] = A;
-            Pos2[j] = A & k3;
-            Pos4[j] = A & k4;
-            Neg2[j] = A & km2;
-            Neg4[j] = A & km4;
-            const int pp = 2 * __popc(Pos2[j]) + 4 * __popc(Pos4[j]);
-            psum += pp;
-            dsum += pp - 2 * __popc(Neg2[j]) - 4 * __popc(Neg4[j]);
           }
         }
-        // ---- block reduction of (dsum, psum): REDUX per warp, one barrier
-        const int wd = (int)__reduce_add_sync(0xffffffffu, (unsigned)dsum);
-        const int wp = (int)__reduce_add_sync(0xffffffffu, (unsigned)psum);
-        int *rb = red + buf * 2 * NWARP;
-        if (lane == 0) {
-          rb[warp] = wd;
-          rb[NWARP + warp] = wp;
-        }
-        __syncthreads();
-        int D = 0, Pt = 0;
-#pragma unroll
-        for (int i = 0; i < NWARP; i++) {
-          D += rb[i];
-          Pt += rb[NWARP + i];
-        }
-        if (Pt > 0) sweep_flipped = true;  // greedy flips are exactly the positive ones
-        if (cur + Pt > best) {
-          // ---- per-word prefix bounds; word order is (j, tid)
-          int wpos[WPT], excl[WPT];
-#pragma unroll
-          for (int j = 0; j < WPT; j++) {
-            wpos[j] = 2 * __popc(Pos2[j]) + 4 * __popc(Pos4[j]);
-            const int ws = wpos[j] - 2 * __popc(Neg2[j]) - 4 * __popc(Neg4[j]);
-            int incl = ws;
+        // ---- pass 2 (SA): warp-cooperative tail.  Undecided sites take bits
+        // 23..0 of their uniform from a per-site Philox word; the warp draws
+        // all pending 4-site groups together, 32 per round.
+        if (SA) {
+          bool any_tail = false;
+#pragma unroll 1
+          while (true) {
+            const int cnt = __popcll(itm);
+            int incl = cnt;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
               const int y = __shfl_up_sync(0xffffffffu, incl, off);
               if (lane >= off) incl += y;
             }
-            excl[j] = incl - ws;
-            if (lane == 31) scan[j * NWARP + warp] = incl;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total == 0) break;
+            any_tail = true;
+            int slot = incl - cnt;
+            while (itm && slot < 32) {
+              const int bpos = __ffsll((long long)itm) - 1;
+              itm &= itm - 1;
+              myq[slot++] = ((uint32_t)lane << 8) | (uint32_t)bpos;
+            }
+            __syncwarp();
+            if (lane < total) {
+              const uint32_t it = myq[lane];
+              const int ol = (int)(it >> 8), jj = (int)((it >> 3) & 7u), gi = (int)(it & 7u);
+              const uint32_t wi = (uint32_t)(jj * NT + warp * 32 + ol);
+              const P4 r = philox10(P4{wi, (uint32_t)t, (uint32_t)(4 + 8 * p + gi), 1u}, key0, key1);
+              const uint32_t en = (teq[jj * 32 + ol] >> (4 * gi)) & 0xFu;
+              const uint32_t cn = (tc2[jj * 32 + ol] >> (4 * gi)) & 0xFu;
+              const uint32_t tw[4] = {r.x, r.y, r.z, r.w};
+              uint32_t ln = 0;
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                const uint32_t klo = ((cn >> q) & 1u) ? K2lo : K4lo;
+                if (((en >> q) & 1u) && (tw[q] >> 8) < klo) ln |= 1u << q;
+              }
+              if (ln) atomicOr(&tlt[jj * 32 + ol], ln << (4 * gi));
+            }
+            __syncwarp();
+          }
+          if (any_tail) {
+#pragma unroll
+            for (int j = 0; j < WPT; j++) {
+              if (eq[j]) {
+                lt[j] |= tlt[j * 32 + lane];
+                tlt[j * 32 + lane] = 0;
+              }
+            }
+          }
+        }
+        // ---- pass 3: commit the flips
+        int dsum = 0, psum = 0;
+#pragma unroll
+        for (int j = 0; j < WPT; j++) {
+          if (own[j]) {
+            const int wi = j * NT + tid;
+            if (SA) {
+              wsum[j] -= 2 * __popc(lt[j] & c2[j]) + 4 * __popc(lt[j] & ~c2[j]);
+              A[j] |= lt[j];
+            }
+            S[p][j] ^= A[j];
+            st[p * nw + wi] = S[p][j];
+            dsum += wsum[j];
+            psum += wpos[j];
+          }
+        }
+        // ---- block reduction of (dsum, psum): REDUX per warp, one barrier
+        const int wd = (int)__reduce_add_sync(0xffffffffu, (unsigned)dsum);
+        const int wp = (int)__reduce_add_sync(0xffffffffu, (unsigned)psum);
+        int D = wd, Pt = wp;
+        if (NWARP > 1) {
+          int *rb = red + buf * 2 * NWARP;
+          if (lane == 0) {
+            rb[warp] = wd;
+            rb[NWARP + warp] = wp;
           }
           __syncthreads();
-          int base = 0;
+          D = 0;
+          Pt = 0;
+#pragma unroll
+          for (int i = 0; i < NWARP; i++) {
+            D += rb[i];
+            Pt += rb[NWARP + i];
+          }
+        } else {
+          __syncwarp();
+        }
+        if (Pt > 0) sweep_flipped = true;  // greedy flips are exactly the positive ones
+        if (cur + Pt > best) {
+          // ---- per-word prefix bounds; word order is (j, warp, lane)
+          int excl[WPT];
+          int rtot[WPT];
+#pragma unroll
+          for (int j = 0; j < WPT; j++) {
+            int incl = wsum[j];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, incl, off);
+              if (lane >= off) incl += y;
+            }
+            excl[j] = incl - wsum[j];
+            rtot[j] = __shfl_sync(0xffffffffu, incl, 31);
+            if (NWARP > 1 && lane == 31) scan[j * NWARP + warp] = incl;
+          }
+          if (NWARP > 1) __syncthreads();
+          int basep = 0;
           bool cand = false;
 #pragma unroll
           for (int j = 0; j < WPT; j++) {
-            int wbase = base;
-            for (int i = 0; i < NWARP; i++) {
-              const int v = scan[j * NWARP + i];
-              if (i < warp) wbase += v;
-              base += v;
+            int wbase = basep;
+            if (NWARP > 1) {
+              for (int i = 0; i < NWARP; i++) {
+                const int v = scan[j * NWARP + i];
+                if (i < warp) wbase += v;
+                basep += v;
+              }
+            } else {
+              basep += rtot[j];
             }
             excl[j] += wbase;
             if (own[j] && wpos[j] > 0 && cur + excl[j] + wpos[j] > best) cand = true;
           }
-          if (__syncthreads_or(cand)) {
+          const bool anyc = NWARP > 1 ? __syncthreads_or(cand) : __any_sync(0xffffffffu, cand);
+          if (anyc) {
             long long key = LLONG_MIN;
 #pragma unroll
             for (int j = 0; j < WPT; j++) {
               if (!own[j] || wpos[j] <= 0 || cur + excl[j] + wpos[j] <= best) continue;
+              // recompute the classes of the pre-phase word (neighbours unchanged)
+              const int wi = j * NT + tid;
+              const uint4 g = geo[wi];
+              const uint32_t Sold = S[p][j] ^ A[j];
+              const uint32_t same = S[p ^ 1][j];
+              const uint32_t sh = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
+                                             p ? (g.z >> 16) : (g.z & 0xFFFFu));
+              const Classes c = classes(Sold, same, sh, o[g.x & 0xFFFFu], o[g.x >> 16],
+                                        msk[p * nw + wi], g.w);
+              const uint32_t Aj = A[j];
+              const uint32_t P2 = Aj & c.k3, P4m = Aj & c.k4, N2 = Aj & c.km2, N4 = Aj & c.km4;
               int v = cur + excl[j], mx = INT_MIN, mp = -1;
-              uint32_t nz = Pos2[j] | Pos4[j] | Neg2[j] | Neg4[j];
+              uint32_t nz = P2 | P4m | N2 | N4;
               while (nz) {
                 const int b = __ffs(nz) - 1;
                 nz &= nz - 1;
                 const uint32_t bm = 1u << b;
-                const int d = (Pos2[j] & bm) ? 2 : (Pos4[j] & bm) ? 4 : (Neg2[j] & bm) ? -2 : -4;
+                const int d = (P2 & bm) ? 2 : (P4m & bm) ? 4 : (N2 & bm) ? -2 : -4;
                 v += d;
                 if (d > 0 && v > mx) {
                   mx = v;
                   mp = b;
                 }
               }
-              const long long pos = (long long)(j * NT + tid) * 32 + mp;
+              const long long pos = (long long)wi * 32 + mp;
               const long long kk = (long long)((unsigned long long)(long long)mx << 32) |
                                    (long long)(0xFFFFFFFFu - (uint32_t)pos);
               key = kk > key ? kk : key;
@@ -371,11 +499,13 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               const long long y = __shfl_xor_sync(0xffffffffu, key, off);
               key = y > key ? y : key;
             }
-            if (lane == 0) kred[warp] = key;
-            __syncthreads();
-            key = LLONG_MIN;
+            if (NWARP > 1) {
+              if (lane == 0) kred[warp] = key;
+              __syncthreads();
+              key = LLONG_MIN;
 #pragma unroll
-            for (int i = 0; i < NWARP; i++) key = kred[i] > key ? kred[i] : key;
+              for (int i = 0; i < NWARP; i++) key = kred[i] > key ? kred[i] : key;
+            }
             const int mval = (int)(key >> 32);
             if (key != LLONG_MIN && mval > best) {
               best = mval;
@@ -385,9 +515,9 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               for (int j = 0; j < WPT; j++) {
                 if (!own[j]) continue;
                 const int wi = j * NT + tid;
-                const uint32_t now = S[p][j], old = now ^ Am[j];
+                const uint32_t now = S[p][j], old = now ^ A[j];
                 const uint32_t snap = wi < wstar    ? now
-                                      : wi == wstar ? old ^ (Am[j] & ((2u << bstar) - 1u))
+                                      : wi == wstar ? old ^ (A[j] & ((2u << bstar) - 1u))
                                                     : old;
                 bst[p * nw + wi] = snap;
                 bst[(p ^ 1) * nw + wi] = S[p ^ 1][j];
@@ -408,10 +538,11 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
     for (int j = 0; j < WPT; j++) {
       if (own[j]) {
         const int wi = j * NT + tid;
+        const uint4 g = geo[wi];
         const uint32_t *o = bst + nw;
         const uint32_t same = o[wi];
-        const uint32_t sh = shifted_nb(o, same, geo[j].cidx[0], geo[j].cinfo[0]);
-        cb += word_cut(bst[wi], same, sh, o[geo[j].up], o[geo[j].dn], msk[wi], vmask[0][j]);
+        const uint32_t sh = shifted_nb(o, same, g.y & 0xFFFFu, g.z & 0xFFFFu);
+        cb += word_cut(bst[wi], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], msk[wi], g.w);
       }
     }
     cb = (int)__reduce_add_sync(0xffffffffu, (unsigned)cb);
@@ -450,7 +581,9 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
 // ------------------------------------------------------------------ launch
 static size_t smem_bytes(int nw, int NT, int WPT) {
   const int NWARP = NT / 32;
-  size_t b = (size_t)2 * nw * 16 + (size_t)4 * nw * 4;
+  size_t b = (size_t)3 * nw * 16;                           // msk, geo
+  b += (size_t)4 * nw * 4;                                  // st, bst
+  b += (size_t)NWARP * 3 * WPT * 32 * 4 + (size_t)NWARP * 32 * 4;  // tail exchange + queue
   b += (size_t)(6 * NWARP) * 4;
   b += (size_t)((WPT * NWARP + 1) & ~1) * 4;
   b += (size_t)NWARP * 8;
@@ -489,13 +622,24 @@ bool checker_fits(int rows, int cols) {
   if ((rows & 1) || (cols & 1) || rows < 4 || cols < 4) return false;
   int WPR, nw;
   checker_words(rows, cols, &WPR, &nw);
-  return nw <= 4096;
+  return nw <= 2048;
 }
 
 size_t checker_workspace_bytes(int rows, int cols) {
   int WPR, nw;
   checker_words(rows, cols, &WPR, &nw);
-  return align_up((size_t)2 * nw * 16, 256) + align_up((size_t)2 * nw * 4, 256);
+  return align_up((size_t)2 * nw * 16, 256) + align_up((size_t)nw * 16, 256);
+}
+
+template <int WPT>
+static int launch_wpt(const CheckerArgs &a, bool sa, int nsm, int W, cudaStream_t stream) {
+  switch (W) {
+    case 1: return launch_nt<32, WPT>(a, sa, nsm, stream);
+    case 2: return launch_nt<64, WPT>(a, sa, nsm, stream);
+    case 4: return launch_nt<128, WPT>(a, sa, nsm, stream);
+    case 8: return launch_nt<256, WPT>(a, sa, nsm, stream);
+    default: return launch_nt<512, WPT>(a, sa, nsm, stream);
+  }
 }
 
 int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
@@ -507,9 +651,9 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   const int nsm = num_sms();
   if (nsm <= 0) return set_error(GSB_ECUDA, "no CUDA device");
   uint4 *masks = (uint4 *)ws;
-  uint32_t *valid = (uint32_t *)((char *)ws + align_up((size_t)2 * nw * 16, 256));
+  uint4 *geo = (uint4 *)((char *)ws + align_up((size_t)2 * nw * 16, 256));
   checker_masks_kernel<<<(2 * nw + 255) / 256, 256, 0, stream>>>(rows, cols, WPR, w_dev, masks,
-                                                                 valid);
+                                                                 geo);
   CheckerArgs a;
   a.rows = rows;
   a.cols = cols;
@@ -518,7 +662,7 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.nw = nw;
   a.lb = (a.H - 1) & 31;
   a.masks = masks;
-  a.valid = valid;
+  a.geo = geo;
   a.table = table;
   a.sweeps = sweeps;
   a.seeds = seeds;
@@ -529,17 +673,20 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.nbytes = (rows * cols + 7) / 8;
   a.err = err_ws;
   const bool sa = kind == GSB_ANNEALING;
-  if (nw <= 32) return launch_nt<32, 1>(a, sa, nsm, stream);
-  if (nw <= 64) return launch_nt<64, 1>(a, sa, nsm, stream);
-  if (nw <= 128) return launch_nt<128, 1>(a, sa, nsm, stream);
-  if (nw <= 224) return launch_nt<224, 1>(a, sa, nsm, stream);
-  if (nw <= 320) return launch_nt<320, 1>(a, sa, nsm, stream);
-  if (nw <= 416) return launch_nt<416, 1>(a, sa, nsm, stream);
-  if (nw <= 512) return launch_nt<512, 1>(a, sa, nsm, stream);
-  if (nw <= 1024) return launch_nt<512, 2>(a, sa, nsm, stream);
-  if (nw <= 2048) return launch_nt<512, 4>(a, sa, nsm, stream);
-  if (nw <= 4096) return launch_nt<512, 8>(a, sa, nsm, stream);
-  return set_error(GSB_EUNSUPPORTED, "torus too large for the shared-memory checkerboard path");
+  // Team shape: W warps per trial (power of two), WPT words per lane.  Aim
+  // for >= ~12 resident warps per SM with as few warps per trial as possible
+  // (cheap barriers, more ILP per lane) and WPT <= 6.
+  int W = 1;
+  while (W < 16 && 32 * W < nw &&
+         ((long long)T * W < 12LL * nsm || (nw + 32 * W - 1) / (32 * W) > 6))
+    W *= 2;
+  const int wpt = (nw + 32 * W - 1) / (32 * W);
+  if (wpt <= 1) return launch_wpt<1>(a, sa, nsm, W, stream);
+  if (wpt <= 2) return launch_wpt<2>(a, sa, nsm, W, stream);
+  if (wpt <= 3) return launch_wpt<3>(a, sa, nsm, W, stream);
+  if (wpt <= 4) return launch_wpt<4>(a, sa, nsm, W, stream);
+  if (wpt <= 6) return launch_wpt<6>(a, sa, nsm, W, stream);
+  return launch_wpt<8>(a, sa, nsm, W, stream);
 }
 
 }  // namespace gsb
