@@ -31,6 +31,7 @@
 // the maximum defines the snapshot (pre-phase words + accepted flips up to it).
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "gsb_device.cuh"
 #include "gsb_internal.h"
@@ -176,9 +177,16 @@ __device__ __forceinline__ uint32_t nibmask8(uint32_t x) {
   return x;
 }
 
+__device__ __forceinline__ int popc_itm(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc_itm(uint64_t x) { return __popcll(x); }
+__device__ __forceinline__ int ffs_itm(uint32_t x) { return __ffs(x); }
+__device__ __forceinline__ int ffs_itm(uint64_t x) { return __ffsll((long long)x); }
+
 template <int NT, int WPT, bool SA>
 __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
   constexpr int NWARP = NT / 32;
+  // tail items (word j, 4-site group g) packed as bit 8j+g
+  using ItmT = typename std::conditional<(WPT <= 4), uint32_t, uint64_t>::type;
   static_assert(WPT <= 8, "tail item index packs 8 words x 8 groups");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = a.nw;
@@ -192,6 +200,7 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
   int *red2 = red + 4 * NWARP;                    // [2][NWARP]
   int *scan = red2 + 2 * NWARP;                   // [WPT][NWARP]
   long long *kred = (long long *)(scan + ((WPT * NWARP + 1) & ~1));  // [NWARP]
+  int *wctrs = (int *)(kred + NWARP);              // [NWARP] tail slot counters
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -199,10 +208,12 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
   uint32_t *tc2 = teq + WPT * 32;            // [WPT][32] class -2 masks
   uint32_t *tlt = tc2 + WPT * 32;            // [WPT][32] accepted-by-tail bits
   uint32_t *myq = tq + warp * 32;
+  int *wctr = wctrs + warp;
 
   for (int i = tid; i < 2 * nw; i += NT) msk[i] = a.masks[i];
   for (int i = tid; i < nw; i += NT) geo[i] = a.geo[i];
   for (int i = tid; i < NWARP * 3 * WPT * 32; i += NT) tx[i] = 0;
+  if (tid < NWARP) wctrs[tid] = 0;
   __syncthreads();
 
   bool own[WPT];
@@ -214,19 +225,20 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
     const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
 
     // ---- initial spins: bit (k&31) of word 0 of Philox(key, (wi, 0, p, 0))
-    uint32_t S[2][WPT];
+    uint32_t cur_w[WPT], oth_w[WPT];  // owned words of the colour being updated / the other
 #pragma unroll
     for (int j = 0; j < WPT; j++) {
       const int wi = j * NT + tid;
-      S[0][j] = S[1][j] = 0;
+      cur_w[j] = oth_w[j] = 0;
       if (own[j]) {
         const uint32_t V = geo[wi].w;
 #pragma unroll
         for (int p = 0; p < 2; p++) {
           const P4 o = philox10(P4{(uint32_t)wi, 0u, (uint32_t)p, 0u}, key0, key1);
-          S[p][j] = o.x & V;
-          st[p * nw + wi] = S[p][j];
-          bst[p * nw + wi] = S[p][j];
+          const uint32_t s0 = o.x & V;
+          if (p == 0) cur_w[j] = s0; else oth_w[j] = s0;
+          st[p * nw + wi] = s0;
+          bst[p * nw + wi] = s0;
         }
       }
     }
@@ -240,8 +252,8 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
         const int wi = j * NT + tid;
         const uint4 g = geo[wi];
         const uint32_t *o = st + nw;
-        const uint32_t sh = shifted_nb(o, S[1][j], g.y & 0xFFFFu, g.z & 0xFFFFu);
-        c0 += word_cut(S[0][j], S[1][j], sh, o[g.x & 0xFFFFu], o[g.x >> 16], msk[wi], g.w);
+        const uint32_t sh = shifted_nb(o, oth_w[j], g.y & 0xFFFFu, g.z & 0xFFFFu);
+        c0 += word_cut(cur_w[j], oth_w[j], sh, o[g.x & 0xFFFFu], o[g.x >> 16], msk[wi], g.w);
       }
     }
     c0 = (int)__reduce_add_sync(0xffffffffu, (unsigned)c0);
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
         const uint32_t *o = st + (p ^ 1) * nw;
         uint32_t A[WPT], c2[WPT], eq[WPT], lt[WPT];
         int wpos[WPT], wsum[WPT];
-        uint64_t itm = 0;
+        ItmT itm = 0;
         // ---- pass 1: classes and the unconditional planes 0-7
 #pragma unroll
         for (int j = 0; j < WPT; j++) {
@@ -288,10 +300,10 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
           if (own[j]) {
             const uint4 g = geo[wi];
             const uint4 m = msk[p * nw + wi];
-            const uint32_t same = S[p ^ 1][j];
+            const uint32_t same = oth_w[j];
             const uint32_t sh = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
                                            p ? (g.z >> 16) : (g.z & 0xFFFFu));
-            const Classes c = classes(S[p][j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m, g.w);
+            const Classes c = classes(cur_w[j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m, g.w);
             wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
             if (SA) {
               uint32_t b = c.ge2;
@@ -327,7 +339,7 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               if (q) {
                 teq[j * 32 + lane] = q;
                 tc2[j * 32 + lane] = e2;
-                itm |= (uint64_t)nibmask8(q) << (8 * j);
+                itm |= (ItmT)nibmask8(q) << (8 * j);
               }
             } else {
               A[j] = c.k3 | c.k4;
@@ -342,19 +354,15 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
           bool any_tail = false;
 #pragma unroll 1
           while (true) {
-            const int cnt = __popcll(itm);
-            int incl = cnt;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, incl, off);
-              if (lane >= off) incl += y;
-            }
-            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            const int cnt = popc_itm(itm);
+            const int sbase = cnt ? atomicAdd(wctr, cnt) : 0;
+            __syncwarp();
+            const int total = *wctr;
             if (total == 0) break;
             any_tail = true;
-            int slot = incl - cnt;
+            int slot = sbase;
             while (itm && slot < 32) {
-              const int bpos = __ffsll((long long)itm) - 1;
+              const int bpos = ffs_itm(itm) - 1;
               itm &= itm - 1;
               myq[slot++] = ((uint32_t)lane << 8) | (uint32_t)bpos;
             }
@@ -375,6 +383,8 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               }
               if (ln) atomicOr(&tlt[jj * 32 + ol], ln << (4 * gi));
             }
+            __syncwarp();
+            if (lane == 0) *wctr = 0;
             __syncwarp();
           }
           if (any_tail) {
@@ -397,8 +407,8 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               wsum[j] -= 2 * __popc(lt[j] & c2[j]) + 4 * __popc(lt[j] & ~c2[j]);
               A[j] |= lt[j];
             }
-            S[p][j] ^= A[j];
-            st[p * nw + wi] = S[p][j];
+            cur_w[j] ^= A[j];
+            st[p * nw + wi] = cur_w[j];
             dsum += wsum[j];
             psum += wpos[j];
           }
@@ -468,8 +478,8 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               // recompute the classes of the pre-phase word (neighbours unchanged)
               const int wi = j * NT + tid;
               const uint4 g = geo[wi];
-              const uint32_t Sold = S[p][j] ^ A[j];
-              const uint32_t same = S[p ^ 1][j];
+              const uint32_t Sold = cur_w[j] ^ A[j];
+              const uint32_t same = oth_w[j];
               const uint32_t sh = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
                                              p ? (g.z >> 16) : (g.z & 0xFFFFu));
               const Classes c = classes(Sold, same, sh, o[g.x & 0xFFFFu], o[g.x >> 16],
@@ -515,17 +525,23 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
               for (int j = 0; j < WPT; j++) {
                 if (!own[j]) continue;
                 const int wi = j * NT + tid;
-                const uint32_t now = S[p][j], old = now ^ A[j];
+                const uint32_t now = cur_w[j], old = now ^ A[j];
                 const uint32_t snap = wi < wstar    ? now
                                       : wi == wstar ? old ^ (A[j] & ((2u << bstar) - 1u))
                                                     : old;
                 bst[p * nw + wi] = snap;
-                bst[(p ^ 1) * nw + wi] = S[p ^ 1][j];
+                bst[(p ^ 1) * nw + wi] = oth_w[j];
               }
             }
           }
         }
         cur += D;
+#pragma unroll
+        for (int j = 0; j < WPT; j++) {  // next phase updates the other colour
+          const uint32_t tmp = cur_w[j];
+          cur_w[j] = oth_w[j];
+          oth_w[j] = tmp;
+        }
       }
       executed = t + 1;
       if (!SA && !sweep_flipped) break;
@@ -586,7 +602,7 @@ static size_t smem_bytes(int nw, int NT, int WPT) {
   b += (size_t)NWARP * 3 * WPT * 32 * 4 + (size_t)NWARP * 32 * 4;  // tail exchange + queue
   b += (size_t)(6 * NWARP) * 4;
   b += (size_t)((WPT * NWARP + 1) & ~1) * 4;
-  b += (size_t)NWARP * 8;
+  b += (size_t)NWARP * 8 + (size_t)NWARP * 4;
   return b;
 }
 
