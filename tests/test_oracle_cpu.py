@@ -1,0 +1,175 @@
+"""Pin the CPU oracle (oracle/gsb_oracle.c) against outputs of the reference.
+
+Every fixture under tests/golden/ was produced by running the unmodified
+Python reference (tests/golden/make_golden.py) or torch's Philox header
+(oracle/tools/make_philox_kat.sh).  CPU only.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden, hex_to_spins
+
+
+def test_mix_seed_kats(oracle):
+    for m, i, v in golden("rng_kat.json")["mix_seed"]:
+        assert oracle.mix_seed(m, i) == v
+    # the reference's own KAT (test_campaign.py:44-50)
+    assert [oracle.mix_seed(1234567, i) for i in range(3)] == [
+        6457827717110365317, 3203168211198807973, 9817491932198370423]
+
+
+def test_seedsequence_pcg64_init(oracle):
+    for seed, st in golden("rng_kat.json")["pcg64_init"]:
+        s, inc = oracle.Pcg64(seed).state
+        assert (hex(s), hex(inc)) == (st["state"], st["inc"]), seed
+
+
+def test_pcg64_stream_consumption(oracle):
+    for rec in golden("rng_kat.json")["streams"]:
+        g = oracle.Pcg64(rec["seed"])
+        assert [g.next64() for _ in range(6)] == rec["next64"]
+        g = oracle.Pcg64(rec["seed"])
+        assert [g.next32() >> 31 for _ in range(13)] == rec["integers_0_2_13"]
+        assert list(g.permutation(37)) == rec["perm_37"]
+        assert [g.random().hex() for _ in range(3)] == rec["random_3"]
+        assert list(g.permutation(5)) == rec["perm_5"]
+        assert (g._s.has_uint32, g._s.uinteger) == (rec["has_uint32"], rec["uinteger"])
+
+
+def test_philox_against_torch_and_random123(oracle):
+    for c in golden("philox_kat.json")["cases"]:
+        assert oracle.philox(c["ctr"], c["key"]) == c["out"]
+    # Random123 known-answer vectors (kat_vectors, philox4x32 10)
+    assert oracle.philox([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert oracle.philox([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2) == [
+        0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert oracle.philox([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+                         [0xA4093822, 0x299F31D0]) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420,
+                                                       0x24126EA1]
+
+
+def test_torus_weights_and_evaluator(oracle):
+    for rec in golden("tori.json")["tori"]:
+        w = oracle.torus_weights(rec["rows"], rec["cols"], rec["seed"])
+        assert hashlib.sha256(w.tobytes()).hexdigest() == rec["w_sha256"]
+        assert int(w.astype(np.int64).sum()) == rec["total_weight"]
+        if "w" in rec:
+            assert w.tolist() == rec["w"]
+        if "evals" not in rec:
+            continue
+        eu, ev, ew = oracle.torus_edges(rec["rows"], rec["cols"], w)
+        for e in rec["evals"]:
+            s = hex_to_spins(e["hex"], rec["n"])
+            assert oracle.cut(eu, ev, ew, s) == e["cut"]
+            assert oracle.energy(eu, ev, ew, s) == e["energy"]
+            assert e["energy"] == rec["total_weight"] - 2 * e["cut"]  # evaluate.py:10-12
+
+
+def test_codec_restatement(oracle):
+    for c in golden("codec.json")["cases"]:
+        assert oracle.encode_hex(np.array(c["spins"])) == c["hex"]
+
+
+def _trial_rows_check(oracle, rows, cols, tseed, recs):
+    w = oracle.torus_weights(rows, cols, tseed)
+    eu, ev, ew = oracle.torus_edges(rows, cols, w)
+    for r in recs:
+        bc, bs, se = oracle.run_trials_ref(rows * cols, eu, ev, ew, r["kind"], r["sweeps"],
+                                           [r["seed"]], r.get("temp_start"), r.get("temp_end"))
+        assert (int(bc[0]), int(se[0]), oracle.encode_hex(bs[0])) == (
+            r["best_cut"], r["sweeps_executed"], r["hex"]), r
+
+
+def test_reference_trials_small_tori(oracle):
+    rows = golden("trials_small.json")["trials"]
+    groups = {}
+    for r in rows:
+        groups.setdefault((r["rows"], r["cols"], r["torus_seed"]), []).append(r)
+    for (R, C, s), rs in groups.items():
+        _trial_rows_check(oracle, R, C, s, rs)
+
+
+def test_reference_trials_random_graphs(oracle):
+    for g in golden("graphs_small.json")["graphs"]:
+        E = np.array(g["edges"])
+        eu, ev, ew = (E[:, 0] - 1).astype(np.int32), (E[:, 1] - 1).astype(np.int32), E[:, 2]
+        for r in g["runs"]:
+            t0, t1 = (3.0, 0.05) if r["kind"] == "simulated_annealing" else (0.0, 0.0)
+            bc, bs, se = oracle.run_trials_ref(g["n"], eu, ev, ew, r["kind"], r["sweeps"],
+                                               [r["seed"]], t0, t1)
+            assert (int(bc[0]), int(se[0]), oracle.encode_hex(bs[0])) == (
+                r["best_cut"], r["sweeps_executed"], r["hex"])
+
+
+@pytest.mark.parametrize("name", ["c1_full", "c2_sample"])
+def test_reference_trials_baseline_configs(oracle, name):
+    """BASELINE config 1 (all 100 SA + 100 greedy trials) and config 2 (8 full trials)."""
+    c = golden(f"{name}.json")
+    w = oracle.torus_weights(c["rows"], c["cols"], 1)
+    eu, ev, ew = oracle.torus_edges(c["rows"], c["cols"], w)
+    n = c["rows"] * c["cols"]
+    for kind, run in c["runs"].items():
+        tr = run["trials"]
+        t0, t1 = (3.0, 0.05) if kind == "simulated_annealing" else (0.0, 0.0)
+        bc, bs, se = oracle.run_trials_ref(n, eu, ev, ew, kind, c["sweeps"],
+                                           [r["seed"] for r in tr], t0, t1)
+        for i, r in enumerate(tr):
+            assert (int(bc[i]), int(se[i]), oracle.encode_hex(bs[i])) == (
+                r["best_cut"], r["sweeps_executed"], r["hex"]), (name, kind, r["index"])
+
+
+@pytest.mark.parametrize("name,k", [("c3_sample", 1), ("c4_sample", 8)])
+def test_reference_trials_large_configs(oracle, name, k):
+    """Configs 3/4 full-length samples; c4 (67 s/trial) only with GSB_SLOW=1."""
+    if name == "c4_sample" and not os.environ.get("GSB_SLOW"):
+        pytest.skip("set GSB_SLOW=1 for the 8 full-length config-4 trials (~70 s on 8 cores)")
+    c = golden(f"{name}.json")
+    w = oracle.torus_weights(c["rows"], c["cols"], 1)
+    eu, ev, ew = oracle.torus_edges(c["rows"], c["cols"], w)
+    tr = c["runs"]["simulated_annealing"]["trials"][:k]
+    bc, bs, se = oracle.run_trials_ref(c["rows"] * c["cols"], eu, ev, ew, "simulated_annealing",
+                                       c["sweeps"], [r["seed"] for r in tr], 3.0, 0.05)
+    for i, r in enumerate(tr):
+        assert (int(bc[i]), int(se[i]), oracle.encode_hex(bs[i])) == (
+            r["best_cut"], r["sweeps_executed"], r["hex"])
+
+
+def test_checker_oracle_properties(oracle):
+    """Checkerboard oracle: deterministic, best matches recomputed cut, greedy local optimum."""
+    rows, cols = 8, 10
+    w = oracle.torus_weights(rows, cols, 3)
+    eu, ev, ew = oracle.torus_edges(rows, cols, w)
+    seeds = [oracle.mix_seed(20250814, i) for i in range(5)]
+    a = oracle.run_trials_checker(rows, cols, w, "simulated_annealing_checkerboard", 50, seeds,
+                                  3.0, 0.05)
+    b = oracle.run_trials_checker(rows, cols, w, "simulated_annealing_checkerboard", 50, seeds,
+                                  3.0, 0.05)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for i in range(5):
+        assert oracle.cut(eu, ev, ew, a[1][i]) == a[0][i]
+    g = oracle.run_trials_checker(rows, cols, w, "greedy_checkerboard", 10_000, seeds)
+    for i in range(5):
+        s = g[1][i].astype(np.int64)
+        assert g[2][i] < 10_000
+        base = oracle.cut(eu, ev, ew, g[1][i])
+        for v in range(rows * cols):  # no single flip improves a greedy optimum
+            t = g[1][i].copy()
+            t[v] = -t[v]
+            assert oracle.cut(eu, ev, ew, t) <= base
+        del s
+
+
+def test_checker_oracle_statistically_matches_reference(oracle):
+    """Crit. 6 fixture (test_acceptance.py:255-278): torus 4x4 seed 1, SA 50 sweeps,
+    100 trials, master 20250814 -> reference reaches the optimum 10 in 99/100.
+    The checkerboard kind must also reach it in >= 80/100 (the criterion's bar)."""
+    w = oracle.torus_weights(4, 4, 1)
+    seeds = [oracle.mix_seed(20250814, i) for i in range(100)]
+    bc, _, _ = oracle.run_trials_checker(4, 4, w, "simulated_annealing_checkerboard", 50, seeds,
+                                         3.0, 0.05, spins=False)
+    assert int((bc >= 10).sum()) >= 80
+    assert int(bc.max()) == 10
