@@ -347,6 +347,25 @@ def main():
                "ms_per_step": tot_e2e / a.steps * 1e3,
                "api": "gsb_torus_sweep_host (include/gsb.h)"}
 
+    # ---- Philox blocks the contract required in one step, and this GPU's
+    # pure Philox4x32-10 block rate (live microbenchmark) -> int roofline
+    blocks = np.zeros(1, dtype=np.uint64)
+    _lib.check(L.gsb_workspace_counters(ws.data_ptr(), sp, blocks.ctypes.data))
+    blocks_per_step = int(blocks[0])
+    sink = torch.zeros(256, dtype=torch.int32, device=dev)
+    nthr = nsm_dev = torch.cuda.get_device_properties(dev).multi_processor_count
+    nthr = nsm_dev * 8 * 256
+    bpt = 4096
+    _lib.check(L.gsb_philox_bench(64, sink.data_ptr(), sp))
+    torch.cuda.synchronize()
+    pe0 = torch.cuda.Event(enable_timing=True)
+    pe1 = torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    _lib.check(L.gsb_philox_bench(bpt, sink.data_ptr(), sp))
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    philox_peak = nthr * bpt / (pe0.elapsed_time(pe1) / 1e3)  # blocks/s
+
     # ---- roofline of the dominant kernel (the sweep kernel)
     peaks = {}
     try:
@@ -358,18 +377,26 @@ def main():
     smem_peak = nsm * 128 * f_max  # B/s, 128 B/clk/SM crossbar
     b_alg = 1.25  # bit-packed 5-point stencil: 10 bits per update
     achieved_bw = kernel_rate * b_alg
+    launch_s = tot_kern / a.steps / 1e3
+    rng_achieved = blocks_per_step / launch_s
     roofline = {
-        "bound": "smem", "unit": "GB/s",
-        "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9,
-        "frac": achieved_bw / smem_peak, "traffic": None,
+        "bound": "int", "unit": "Gblock/s (Philox4x32-10)",
+        "achieved": rng_achieved / 1e9, "peak": philox_peak / 1e9,
+        "frac": rng_achieved / philox_peak, "traffic": None,
         "kernel": "gsb::checker_sweep_kernel",
-        "algorithmic_bytes_per_update": b_alg,
+        "algorithmic_units_per_launch": blocks_per_step,
+        "unit_def": "Philox4x32-10 blocks the checkerboard contract requires (2 init + 8 "
+                    "planes per word and half-sweep + per-site tail groups), counted by the kernel",
+        "peak_basis": "measured live: gsb_philox_bench, SMs x 8 x 256 threads evaluating "
+                      "independent Philox4x32-10 blocks (uniform key), CUDA events",
         "updates_per_launch": upd_per_step_rank,
-        "launch_ms": tot_kern / a.steps,
-        "peak_basis": f"{nsm} SMs x 128 B/clk x sm_max {f_max / 1e6:.0f} MHz (computed, "
-                      "no measured SMEM peak in MEASURED_PEAKS.json)",
-        "note": "kernel is integer-issue bound (Philox4x32-10 + bit-sliced stencil); "
-                "see DESIGN.md and profiles/ for the int-issue figures",
+        "launch_ms": launch_s * 1e3,
+        "updates_per_s": kernel_rate,
+        "smem": {"unit": "GB/s", "algorithmic_bytes_per_update": b_alg,
+                 "achieved": achieved_bw / 1e9, "peak": smem_peak / 1e9,
+                 "frac": achieved_bw / smem_peak,
+                 "peak_basis": f"{nsm} SMs x 128 B/clk x sm_max {f_max / 1e6:.0f} MHz (computed; "
+                               "no measured SMEM peak in MEASURED_PEAKS.json)"},
     }
 
     cpu = None

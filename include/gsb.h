@@ -114,6 +114,15 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
  * used this workspace. */
 int gsb_workspace_status(const void *workspace_dev, void *stream);
 
+/* Statistics of the last checkerboard sweep on this workspace: the number of
+ * Philox4x32-10 blocks the contract required (init + 8 planes per word and
+ * half-sweep + the per-site tail groups).  Synchronises `stream`. */
+int gsb_workspace_counters(const void *workspace_dev, void *stream, uint64_t *philox_blocks);
+
+/* Philox4x32-10 throughput probe (roofline denominator): launches
+ * SMs x 8 x 256 threads, each evaluating blocks_per_thread blocks. */
+int gsb_philox_bench(int64_t blocks_per_thread, uint32_t *sink_dev, void *stream);
+
 /* reference engine on a general graph (any integer weights, dmax = max_i sum_j |w_ij|) */
 size_t gsb_graph_workspace_bytes(const gsb_graph *g, int32_t sweeps, int32_t T);
 int gsb_graph_sweep(const gsb_graph *g, int kind, int32_t sweeps, const uint64_t *table_dev,

@@ -161,7 +161,7 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   int *err = (int *)ws;
   char *rest = (char *)ws + err_bytes();
   size_t rest_bytes = ws_bytes - err_bytes();
-  if (cudaMemsetAsync(err, 0, sizeof(int), stream) != cudaSuccess)
+  if (cudaMemsetAsync(err, 0, 16, stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
   int rc;
   if (engine == GSB_ENGINE_CHECKERBOARD) {
@@ -179,6 +179,21 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     return set_error(GSB_EINVAL, "unknown engine");
   }
   return rc;
+}
+
+int gsb_workspace_counters(const void *ws, void *stream, uint64_t *philox_blocks) {
+  if (!ws || !philox_blocks) return set_error(GSB_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(philox_blocks, (const char *)ws + 8, 8, cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return set_error(GSB_ECUDA, cudaGetErrorString(cudaGetLastError()));
+  return GSB_OK;
+}
+
+int gsb_philox_bench(int64_t blocks_per_thread, uint32_t *sink_dev, void *stream) {
+  if (blocks_per_thread < 1 || !sink_dev) return set_error(GSB_EINVAL, "bad arguments");
+  return philox_bench(blocks_per_thread, sink_dev, (cudaStream_t)stream);
 }
 
 int gsb_workspace_status(const void *ws, void *stream) {

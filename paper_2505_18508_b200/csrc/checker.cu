@@ -108,6 +108,7 @@ struct CheckerArgs {
   uint8_t *best_bits;
   int nbytes;
   int *err;
+  unsigned long long *blocks;  // Philox blocks drawn (statistics, workspace)
 };
 
 __device__ __forceinline__ uint32_t shifted_nb(const uint32_t *__restrict__ o, uint32_t same,
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
 #pragma unroll
   for (int j = 0; j < WPT; j++) own[j] = j * NT + tid < nw;
 
+  unsigned tail_blocks = 0;
   for (int trial = blockIdx.x; trial < a.T; trial += gridDim.x) {
     const uint64_t seed = a.seeds[trial];
     const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
             __syncwarp();
             const int total = *wctr;
             if (total == 0) break;
+            tail_blocks += (unsigned)min(total, 32);
             any_tail = true;
             int slot = sbase;
             while (itm && slot < 32) {
@@ -572,6 +575,16 @@ __global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
       a.sweeps_exec[trial] = executed;
       if (cbest != best) atomicExch(a.err, GSB_EINTEGRITY);
     }
+    {
+      // Philox blocks of this trial: 2 init + 2 plane blocks per word and
+      // half-sweep (SA) + the cooperative tail groups
+      unsigned long long nb = (unsigned long long)tail_blocks;
+      nb = __reduce_add_sync(0xffffffffu, lane == 0 ? (unsigned)nb : 0u);
+      if (lane == 0 && nb) atomicAdd(a.blocks, nb);
+      if (tid == 0)
+        atomicAdd(a.blocks, 2ull * nw + (SA ? 4ull * nw * (unsigned long long)executed : 0ull));
+      tail_blocks = 0;
+    }
     // ---- pack best spins MSB-first by site id
     uint8_t *out = a.best_bits + (size_t)trial * a.nbytes;
     const int n = a.rows * a.cols;
@@ -688,6 +701,7 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.best_bits = best_bits;
   a.nbytes = (rows * cols + 7) / 8;
   a.err = err_ws;
+  a.blocks = (unsigned long long *)((char *)err_ws + 8);
   const bool sa = kind == GSB_ANNEALING;
   // Team shape: W warps per trial (power of two), WPT words per lane.  Aim
   // for >= ~12 resident warps per SM with as few warps per trial as possible

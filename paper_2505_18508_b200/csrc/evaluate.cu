@@ -147,4 +147,31 @@ int best_key(const int64_t *best_cut, int T, int64_t first, int64_t *key, cudaSt
   return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
 }
 
+// Philox4x32-10 throughput microbenchmark: every thread evaluates
+// `blocks_per_thread` independent blocks (4 streams interleaved for ILP) and
+// XOR-folds the outputs.  Grid = SMs x 8 CTAs x 256 threads.
+__global__ void __launch_bounds__(256) philox_bench_kernel(int64_t n, uint32_t *sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t k0 = 0x12345678u ^ blockIdx.x, k1 = 0x9abcdef0u;  // uniform key, as in a trial
+  uint32_t acc = 0;
+  for (int64_t i = 0; i < n; i += 4) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const P4 r = philox10(P4{tid, (uint32_t)(i + q), 7u, 1u}, k0, k1);
+      acc ^= r.x ^ r.y ^ r.z ^ r.w;
+    }
+  }
+  if (acc == 0x8badf00du) sink[tid & 255] = acc;  // keep the work alive
+}
+
+int philox_bench_threads() { return num_sms() * 8 * 256; }
+
+int philox_bench(int64_t blocks_per_thread, uint32_t *sink, cudaStream_t stream) {
+  const int nsm = num_sms();
+  if (nsm <= 0) return set_error(GSB_ECUDA, "no CUDA device");
+  philox_bench_kernel<<<nsm * 8, 256, 0, stream>>>(blocks_per_thread, sink);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
+}
+
 }  // namespace gsb
