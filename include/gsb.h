@@ -50,6 +50,8 @@ extern "C" {
 /* engines */
 #define GSB_ENGINE_REFERENCE 0    /* numpy-PCG64 + random permutation: bit-exact with run_trial */
 #define GSB_ENGINE_CHECKERBOARD 1 /* Philox4x32-10 + colour order (DESIGN.md contract)        */
+#define GSB_ENGINE_CHECKERBOARD_TILED 2 /* same contract, forces the HBM-tiled engine (used
+                                           automatically when the torus exceeds shared memory) */
 
 typedef struct gsb_torus {
     int32_t rows, cols;  /* TorusSpec.rows/cols (instances.py:186-187), >= 3 */

@@ -24,6 +24,7 @@ GSB_GREEDY = 0
 GSB_ANNEALING = 1
 ENGINE_REFERENCE = 0
 ENGINE_CHECKERBOARD = 1
+ENGINE_CHECKERBOARD_TILED = 2
 
 _lock = threading.Lock()
 _lib = None

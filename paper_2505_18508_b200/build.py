@@ -15,8 +15,8 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libgsb_cuda.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["abi.cu", "checker.cu", "refexact.cu", "evaluate.cu"]
-HEADERS = ["gsb_device.cuh", "gsb_internal.h"]
+SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "refexact.cu", "evaluate.cu"]
+HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

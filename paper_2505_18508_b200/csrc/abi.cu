@@ -103,7 +103,7 @@ int gsb_schedule_table(int engine, int32_t sweeps, double t0, double t1, int32_t
   int bits;
   if (engine == GSB_ENGINE_REFERENCE)
     bits = 53;
-  else if (engine == GSB_ENGINE_CHECKERBOARD)
+  else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED)
     bits = 32;
   else
     return set_error(GSB_EINVAL, "unknown engine");
@@ -124,8 +124,10 @@ size_t gsb_torus_workspace_bytes(const gsb_torus *inst, int engine, int32_t swee
   if (!inst) return 0;
   int n = inst->rows * inst->cols;
   size_t b = err_bytes();
-  if (engine == GSB_ENGINE_CHECKERBOARD) {
+  if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
     b += checker_workspace_bytes(inst->rows, inst->cols);
+  } else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED) {
+    b += checker_hbm_workspace_bytes(inst->rows, inst->cols, T, num_sms());
   } else {
     b += ref_workspace_bytes(n, 0, T);
   }
@@ -164,14 +166,19 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   if (cudaMemsetAsync(err, 0, 16, stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
   int rc;
-  if (engine == GSB_ENGINE_CHECKERBOARD) {
+  if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED) {
     if ((inst->rows & 1) || (inst->cols & 1))
       return set_error(GSB_EUNSUPPORTED,
                        "checkerboard kinds need even torus dimensions (bipartite torus)");
-    if (!checker_fits(inst->rows, inst->cols))
-      return set_error(GSB_EUNSUPPORTED, "torus too large for the shared-memory engine");
-    rc = checker_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
-                     sweeps_exec, best_bits, rest, err, stream);
+    if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
+      rc = checker_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
+                       best_cut, sweeps_exec, best_bits, rest, err, stream);
+    } else if (checker_hbm_fits(inst->rows, inst->cols)) {
+      rc = checker_hbm_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
+                           best_cut, sweeps_exec, best_bits, rest, err, stream);
+    } else {
+      return set_error(GSB_EUNSUPPORTED, "torus too large for the checkerboard engines");
+    }
   } else if (engine == GSB_ENGINE_REFERENCE) {
     rc = ref_run_torus(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, 4, seeds, T,
                        best_cut, sweeps_exec, best_bits, rest, rest_bytes, err, stream);

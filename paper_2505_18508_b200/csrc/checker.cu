@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "checker_common.cuh"
 #include "gsb_device.cuh"
 #include "gsb_internal.h"
 
@@ -110,73 +111,6 @@ struct CheckerArgs {
   int *err;
   unsigned long long *blocks;  // Philox blocks drawn (statistics, workspace)
 };
-
-__device__ __forceinline__ uint32_t shifted_nb(const uint32_t *__restrict__ o, uint32_t same,
-                                               uint32_t cidx, uint32_t cinfo) {
-  const uint32_t src = cinfo & 31u, dst = (cinfo >> 5) & 31u;
-  const uint32_t carry = ((o[cidx] >> src) & 1u) << dst;
-  return ((cinfo >> 10) & 1u) ? ((same >> 1) | carry) : ((same << 1) | carry);
-}
-
-// cut contribution of a colour-0 word: sum over its 4 edges of w*[differ]
-__device__ __forceinline__ int word_cut(uint32_t s, uint32_t same, uint32_t sh, uint32_t up,
-                                        uint32_t dn, uint4 m, uint32_t v) {
-  int c = 0;
-  uint32_t x;
-  x = (s ^ same) & v;
-  c += __popc(x & ~m.x) - __popc(x & m.x);
-  x = (s ^ sh) & v;
-  c += __popc(x & ~m.y) - __popc(x & m.y);
-  x = (s ^ up) & v;
-  c += __popc(x & ~m.z) - __popc(x & m.z);
-  x = (s ^ dn) & v;
-  c += __popc(x & ~m.w) - __popc(x & m.w);
-  return c;
-}
-
-// Delta classes of a word (bit-sliced counts of the 4 positive-term planes)
-struct Classes {
-  uint32_t ge2, k3, k4, km2, km4;
-};
-
-__device__ __forceinline__ Classes classes(uint32_t Sw, uint32_t same, uint32_t sh, uint32_t up,
-                                           uint32_t dn, uint4 m, uint32_t V) {
-  const uint32_t P0 = ~(Sw ^ same ^ m.x);
-  const uint32_t P1 = ~(Sw ^ sh ^ m.y);
-  const uint32_t P2 = ~(Sw ^ up ^ m.z);
-  const uint32_t P3 = ~(Sw ^ dn ^ m.w);
-  const uint32_t x01 = P0 ^ P1, c01 = P0 & P1, x23 = P2 ^ P3, c23 = P2 & P3;
-  const uint32_t ones = x01 ^ x23;
-  Classes c;
-  c.ge2 = (c01 | c23 | (x01 & x23)) & V;  // Delta >= 0
-  c.k4 = c01 & c23 & V;                    // Delta = +4
-  c.k3 = ((c01 | c23) & ones) & V;         // Delta = +2
-  const uint32_t any = P0 | P1 | P2 | P3;
-  c.km2 = any & ~c.ge2 & V;  // Delta = -2
-  c.km4 = ~any & V;          // Delta = -4
-  return c;
-}
-
-// MSB-first bit-sliced compare step for one plane.  c2 = class -2 sites
-// (threshold K2), other pending sites use K4; ma/mb = all-ones iff the
-// plane's bit of K2/K4 is set (per sweep, uniform).  4 LOP3 per plane.
-__device__ __forceinline__ void cmp_plane(uint32_t R, uint32_t c2, uint32_t ma, uint32_t mb,
-                                          uint32_t &eq, uint32_t &lt) {
-  const uint32_t tb = (c2 & ma) | (~c2 & mb);
-  lt |= eq & ~R & tb;
-  eq &= ~(R ^ tb);
-}
-
-// 8-bit mask of the non-zero nibbles of x (bit g <-> nibble g)
-__device__ __forceinline__ uint32_t nibmask8(uint32_t x) {
-  x |= x >> 1;
-  x |= x >> 2;
-  x &= 0x11111111u;
-  x = (x | (x >> 3)) & 0x03030303u;
-  x = (x | (x >> 6)) & 0x000F000Fu;
-  x = (x | (x >> 12)) & 0xFFu;
-  return x;
-}
 
 __device__ __forceinline__ int popc_itm(uint32_t x) { return __popc(x); }
 __device__ __forceinline__ int popc_itm(uint64_t x) { return __popcll(x); }
@@ -719,4 +653,12 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   return launch_wpt<8>(a, sa, nsm, W, stream);
 }
 
+}  // namespace gsb
+
+namespace gsb {
+void checker_masks_kernel_launch(int rows, int cols, int WPR, const int8_t *w, uint4 *masks,
+                                 uint4 *geo, cudaStream_t stream) {
+  const int nw = rows * WPR;
+  checker_masks_kernel<<<(2 * nw + 255) / 256, 256, 0, stream>>>(rows, cols, WPR, w, masks, geo);
+}
 }  // namespace gsb

@@ -21,6 +21,16 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                 int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                 cudaStream_t stream);
 
+void checker_masks_kernel_launch(int rows, int cols, int WPR, const int8_t *w, uint4 *masks,
+                                 uint4 *geo, cudaStream_t stream);
+// HBM-tiled checkerboard engine (checker_hbm.cu)
+bool checker_hbm_fits(int rows, int cols);
+size_t checker_hbm_workspace_bytes(int rows, int cols, int T, int nsm);
+int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+                    const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
+                    int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
+                    cudaStream_t stream);
+
 // reference-exact engine (refexact.cu)
 size_t ref_workspace_bytes(int n, int64_t m_adj, int T);
 int ref_run_torus(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,

@@ -154,7 +154,7 @@ def _graph_dmax(instance: ProblemInstance) -> int:
 
 
 def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, device=None,
-                      stream=None, check: bool = True):
+                      stream=None, check: bool = True, engine: int | None = None):
     """Batched trials with device-resident outputs (torch tensors).
 
     ``seeds`` is a uint64-valued sequence or an int64 CUDA tensor holding the
@@ -182,6 +182,9 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
     if T == 0:
         return best, sweeps, bits
     kind = _lib.GSB_ANNEALING if config.annealing else _lib.GSB_GREEDY
+    eng = config.engine if engine is None else engine
+    if engine is not None and (engine == _lib.ENGINE_REFERENCE) != (config.engine == _lib.ENGINE_REFERENCE):
+        raise ValueError("engine override must keep the kind's trial semantics")
     with torch.cuda.device(dev):
         s = stream if stream is not None else torch.cuda.current_stream(dev)
         sp = s.cuda_stream
@@ -190,9 +193,9 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
             ts = _lib.torus_struct(instance.torus.rows, instance.torus.cols, w.data_ptr())
             tab = schedule_table(config, 4)
             tab_d = (torch.from_numpy(tab.view(np.int64)).to(dev) if tab is not None else None)
-            wsb = L.gsb_torus_workspace_bytes(ts, config.engine, config.sweeps, T)
+            wsb = L.gsb_torus_workspace_bytes(ts, eng, config.sweeps, T)
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
-            _lib.check(L.gsb_torus_sweep(ts, config.engine, kind, config.sweeps,
+            _lib.check(L.gsb_torus_sweep(ts, eng, kind, config.sweeps,
                                          tab_d.data_ptr() if tab_d is not None else None,
                                          seeds_d.data_ptr(), T, best.data_ptr(),
                                          sweeps.data_ptr(), bits.data_ptr(), ws.data_ptr(), wsb,
@@ -219,11 +222,18 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
     return best, sweeps, bits
 
 
-def run_trials(instance: ProblemInstance, config: SolverConfig, seeds, device=None) -> TrialBatch:
-    """T independent trials of ``config`` (its seed field is replaced by ``seeds``)."""
+def run_trials(instance: ProblemInstance, config: SolverConfig, seeds, device=None,
+               engine: int | None = None) -> TrialBatch:
+    """T independent trials of ``config`` (its seed field is replaced by ``seeds``).
+
+    ``engine`` may force ENGINE_CHECKERBOARD_TILED (the HBM-tiled engine, same
+    results) for checkerboard kinds; by default the engine follows the kind and
+    the torus size.
+    """
     start = time.perf_counter()
     seeds_np = np.asarray(seeds, dtype=np.uint64)
-    best, sweeps, bits = run_trials_device(instance, config, seeds_np, device=device)
+    best, sweeps, bits = run_trials_device(instance, config, seeds_np, device=device,
+                                           engine=engine)
     out = TrialBatch(instance.n, seeds_np, best.cpu().numpy(), sweeps.cpu().numpy(),
                      bits.cpu().numpy(), 0.0)
     out.wall_time_s = time.perf_counter() - start

@@ -174,3 +174,35 @@ def test_checkerboard_rejects_odd_torus():
 def test_mix_seed_kat():
     assert [mix_seed(1234567, i) for i in range(3)] == [
         6457827717110365317, 3203168211198807973, 9817491932198370423]
+
+
+@pytest.mark.parametrize("R,C,s", [(4, 4, 1), (6, 6, 11), (8, 8, 42), (16, 66, 2), (4, 130, 7),
+                                   (50, 100, 1), (20, 64, 9)])
+def test_tiled_engine_matches_oracle(oracle, R, C, s):
+    """HBM-tiled engine (config-5 path) forced on small tori, against the oracle."""
+    from paper_2505_18508_b200 import _lib
+
+    inst = generate_torus(TorusSpec(R, C, s))
+    w = inst.torus_weights
+    seeds = mix_seeds(MASTER, range(20))
+    for cfg in (default_config(ANNEALING_CHECKERBOARD, 25, 0),
+                default_config(GREEDY_CHECKERBOARD, 200, 0)):
+        b = run_trials(inst, cfg, seeds, engine=_lib.ENGINE_CHECKERBOARD_TILED)
+        bc, bs, se = oracle.run_trials_checker(R, C, w, cfg.kind, cfg.sweeps, seeds,
+                                               cfg.temp_start, cfg.temp_end)
+        for i in range(len(seeds)):
+            assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+                bc[i], se[i], oracle.encode_hex(bs[i])), (cfg.kind, i)
+
+
+def test_config5_tiled_engine_consistency():
+    """2000x2000 (BASELINE config 5): bits evaluate to the reported cuts, and the
+    per-trial results do not depend on the batch."""
+    inst = generate_torus(TorusSpec(2000, 2000, 1))
+    cfg = default_config(ANNEALING_CHECKERBOARD, 6, 0)
+    seeds = mix_seeds(MASTER, range(4))
+    b = run_trials(inst, cfg, seeds)
+    cut, en = cut_energy_batch(inst, b.bits)
+    assert np.array_equal(cut.cpu().numpy(), b.best_cut)
+    b1 = run_trials(inst, cfg, seeds[2:3])
+    assert int(b1.best_cut[0]) == int(b.best_cut[2]) and b1.hex(0) == b.hex(2)
