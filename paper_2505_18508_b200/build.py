@@ -15,7 +15,8 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libgsb_cuda.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "refexact.cu", "evaluate.cu"]
+SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "refexact.cu", "refexact_warp.cu",
+           "evaluate.cu"]
 HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh"]
 
 NVCC_FLAGS = [

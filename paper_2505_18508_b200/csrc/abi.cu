@@ -179,6 +179,9 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     } else {
       return set_error(GSB_EUNSUPPORTED, "torus too large for the checkerboard engines");
     }
+  } else if (engine == GSB_ENGINE_REFERENCE && ref_warp_fits(inst->rows, inst->cols)) {
+    rc = ref_warp_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
+                      sweeps_exec, best_bits, rest, err, stream);
   } else if (engine == GSB_ENGINE_REFERENCE) {
     rc = ref_run_torus(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, 4, seeds, T,
                        best_cut, sweeps_exec, best_bits, rest, rest_bytes, err, stream);

@@ -31,7 +31,12 @@ int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweep
                     int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                     cudaStream_t stream);
 
-// reference-exact engine (refexact.cu)
+// reference-exact engines (refexact.cu: any graph; refexact_warp.cu: tori, n < 2^16)
+bool ref_warp_fits(int rows, int cols);
+int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+                 const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
+                 int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
+                 cudaStream_t stream);
 size_t ref_workspace_bytes(int n, int64_t m_adj, int T);
 int ref_run_torus(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                   const uint64_t *table, int dmax, const uint64_t *seeds, int T,

@@ -166,7 +166,7 @@ __global__ void ref_thread_kernel(G g, int n, int kind, int sweeps, const uint64
 }
 
 size_t ref_workspace_bytes(int n, int64_t m_adj, int T) {
-  size_t b = 0;
+  size_t b = 4096;                        // jump-ahead table of the warp engine
   b += align_up((size_t)T * n, 256);      // spins
   b += align_up((size_t)T * n, 256);      // best
   b += align_up((size_t)T * n * 4, 256);  // permutation

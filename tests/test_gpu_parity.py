@@ -206,3 +206,27 @@ def test_config5_tiled_engine_consistency():
     assert np.array_equal(cut.cpu().numpy(), b.best_cut)
     b1 = run_trials(inst, cfg, seeds[2:3])
     assert int(b1.best_cut[0]) == int(b.best_cut[2]) and b1.hex(0) == b.hex(2)
+
+
+@pytest.mark.parametrize("name", ["c2_sample", "c3_sample", "c4_sample"])
+def test_reference_engine_full_length_configs_bit_exact(name):
+    """BASELINE configs 2-4: 8 full-length SA trials each (10k/20k/50k sweeps)
+    reproduce the reference's own best_cut, bitstring and sweeps_executed."""
+    c = golden(f"{name}.json")
+    inst = generate_torus(TorusSpec(c["rows"], c["cols"], 1))
+    rows = c["runs"][ANNEALING]["trials"]
+    cfg = default_config(ANNEALING, c["sweeps"], 0)
+    b = run_trials(inst, cfg, [r["seed"] for r in rows])
+    for i, r in enumerate(rows):
+        assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+            r["best_cut"], r["sweeps_executed"], r["hex"]), (name, r["index"])
+
+
+def test_reference_engine_config1_all_trials():
+    c1 = golden("c1_full.json")
+    inst = generate_torus(TorusSpec(50, 100, 1))
+    rows = c1["runs"][ANNEALING]["trials"]
+    b = run_trials(inst, default_config(ANNEALING, 1000, 0), [r["seed"] for r in rows])
+    for i, r in enumerate(rows):
+        assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+            r["best_cut"], r["sweeps_executed"], r["hex"]), r["index"]
