@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--sweeps", type=int, default=None, help="override sweeps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ref-engine", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -399,6 +400,28 @@ def main():
                                "no measured SMEM peak in MEASURED_PEAKS.json)"},
     }
 
+    # ---- secondary: the bit-exact reference engine (kinds of the reference)
+    # on the same torus, 1024 trials x 1000 sweeps (its own 3.0->0.05 schedule)
+    ref_engine = None
+    if not a.no_ref_engine:
+        from paper_2505_18508_b200.solvers import run_trials_device
+
+        rcfg = default_config("simulated_annealing", 1000, 0)
+        rseeds = mix_seeds(MASTER, range(first, first + 1024))
+        run_trials_device(inst, rcfg, rseeds[:32], device=dev)
+        torch.cuda.synchronize()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        run_trials_device(inst, rcfg, rseeds, device=dev, check=False)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rt = r0.elapsed_time(r1) / 1e3
+        ref_engine = {"value": 1024 * 1000 * n / rt, "unit": "spin-updates/s",
+                      "workload": f"simulated_annealing (bit-exact numpy-PCG64 + permutation "
+                                  f"engine), torus {rows}x{cols}:1, 1024 trials x 1000 sweeps",
+                      "ms": rt * 1e3}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         rate, cores, sample, dt = cpu_port_rate(rows, cols, S, a.cpu_seconds)
@@ -427,6 +450,7 @@ def main():
             "clocks": clk,
             "roofline": roofline,
             "e2e": e2e,
+            "reference_engine": ref_engine,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

@@ -30,6 +30,7 @@
 // only candidate words run the exact bit-serial maximum; the first position of
 // the maximum defines the snapshot (pre-phase words + accepted flips up to it).
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -644,6 +645,10 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   while (W < 16 && 32 * W < nw &&
          ((long long)T * W < 12LL * nsm || (nw + 32 * W - 1) / (32 * W) > 6))
     W *= 2;
+  if (const char *ov = getenv("GSB_CHECKER_WARPS")) {  // development tuning knob
+    const int w = atoi(ov);
+    if (w == 1 || w == 2 || w == 4 || w == 8 || w == 16) W = w;
+  }
   const int wpt = (nw + 32 * W - 1) / (32 * W);
   if (wpt <= 1) return launch_wpt<1>(a, sa, nsm, W, stream);
   if (wpt <= 2) return launch_wpt<2>(a, sa, nsm, W, stream);
