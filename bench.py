@@ -346,6 +346,7 @@ def main():
         e2e = {"value": upd_per_step_rank * world * a.steps / tot_e2e, "unit": "spin-updates/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": tot_e2e / a.steps * 1e3,
+               "step_ms": [round(x * 1e3, 3) for x in e2e_s],
                "api": "gsb_torus_sweep_host (include/gsb.h)"}
 
     # ---- Philox blocks the contract required in one step, and this GPU's

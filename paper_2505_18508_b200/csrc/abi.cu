@@ -45,6 +45,34 @@ static bool torus_ok(const gsb_torus *t) {
 
 static size_t err_bytes() { return 256; }
 
+// Stream-ordered pool for the host-buffer entry point: keeps its reservation
+// between calls (release threshold = max) so repeated calls do not remap
+// device memory.  One pool per device, created on first use.
+static cudaError_t pool_alloc(void **p, size_t bytes, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)pools.size() <= dev) pools.resize(dev + 1, nullptr);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) return e;
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool = pools[dev];
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pool, stream);
+}
+
 }  // namespace gsb
 
 using namespace gsb;
@@ -271,14 +299,14 @@ int gsb_torus_sweep_host(int32_t rows, int32_t cols, const int8_t *w_host, int e
       goto done;                                                     \
     }                                                                \
   } while (0)
-  GSB_TRY(cudaMallocAsync((void **)&w, (size_t)2 * n, stream));
-  GSB_TRY(cudaMallocAsync((void **)&seeds, sizeof(uint64_t) * T, stream));
-  GSB_TRY(cudaMallocAsync((void **)&bc, sizeof(int64_t) * T, stream));
-  GSB_TRY(cudaMallocAsync((void **)&se, sizeof(int32_t) * T, stream));
-  GSB_TRY(cudaMallocAsync((void **)&bits, nbytes * T, stream));
-  GSB_TRY(cudaMallocAsync(&ws, wsb, stream));
+  GSB_TRY(pool_alloc((void **)&w, (size_t)2 * n, stream));
+  GSB_TRY(pool_alloc((void **)&seeds, sizeof(uint64_t) * T, stream));
+  GSB_TRY(pool_alloc((void **)&bc, sizeof(int64_t) * T, stream));
+  GSB_TRY(pool_alloc((void **)&se, sizeof(int32_t) * T, stream));
+  GSB_TRY(pool_alloc((void **)&bits, nbytes * T, stream));
+  GSB_TRY(pool_alloc(&ws, wsb, stream));
   if (!table.empty()) {
-    GSB_TRY(cudaMallocAsync((void **)&tab, sizeof(uint64_t) * table.size(), stream));
+    GSB_TRY(pool_alloc((void **)&tab, sizeof(uint64_t) * table.size(), stream));
     GSB_TRY(cudaMemcpyAsync(tab, table.data(), sizeof(uint64_t) * table.size(),
                             cudaMemcpyHostToDevice, stream));
   }
