@@ -199,7 +199,8 @@ def main():
 
     from paper_2505_18508_b200 import TorusSpec, _lib, generate_torus
     from paper_2505_18508_b200.campaign import mix_seeds
-    from paper_2505_18508_b200.solvers import SolverConfig, default_config, schedule_table
+    from paper_2505_18508_b200.distributed import reduce_best as reduce_best_dist
+    from paper_2505_18508_b200.solvers import default_config, schedule_table
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -230,8 +231,6 @@ def main():
     sweeps_d = torch.empty(T, dtype=torch.int32, device=dev)
     nbytes = (n + 7) // 8
     bits = torch.empty((T, nbytes), dtype=torch.uint8, device=dev)
-    keys = torch.empty(T, dtype=torch.int64, device=dev)
-    win_bits = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
@@ -244,20 +243,10 @@ def main():
                                      bits.data_ptr(), ws.data_ptr(), wsb, sp))
 
     def reduce_best():
-        _lib.check(L.gsb_best_key(best.data_ptr(), T, first, keys.data_ptr(), sp))
-        kmax, arg = torch.max(keys, dim=0)
-        gkey = kmax.clone()
-        if world > 1:
-            dist.all_reduce(gkey, op=dist.ReduceOp.MAX)
-        # owner of the global winner broadcasts its bitstring
-        gk = int(gkey.item())
-        win_idx = 0xFFFFFFFF - (gk & 0xFFFFFFFF)
-        owner = win_idx // T
-        if owner == rank:
-            win_bits.copy_(bits[win_idx - first])
-        if world > 1:
-            dist.broadcast(win_bits, src=int(owner))
-        return gk >> 32, win_idx
+        # campaign-wide best: key kernel, NCCL all-reduce MAX, owner broadcasts
+        # the winning bitstring (paper_2505_18508_b200.distributed.reduce_best)
+        g = reduce_best_dist(best, bits, first, T * world)
+        return g.best_cut, g.index
 
     def step(ev0=None, ev1=None, kev=None):
         if ev0 is not None:

@@ -7,11 +7,12 @@ visible, every compute entry point raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libgsb_cuda.so"
+LIB_PATH = Path(os.environ["GSB_LIB"]) if os.environ.get("GSB_LIB") else PKG / "libgsb_cuda.so"
 
 GSB_OK = 0
 GSB_EINVAL = -1

@@ -25,7 +25,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("GSB_NVCC_FLAGS", "").split()
 
 
 def nvcc() -> str:

@@ -119,7 +119,11 @@ __device__ __forceinline__ int ffs_itm(uint32_t x) { return __ffs(x); }
 __device__ __forceinline__ int ffs_itm(uint64_t x) { return __ffsll((long long)x); }
 
 template <int NT, int WPT, bool SA>
-__global__ void __launch_bounds__(NT) checker_sweep_kernel(CheckerArgs a) {
+#ifndef GSB_CHECKER_WARPS_PER_SM
+#define GSB_CHECKER_WARPS_PER_SM 16
+#endif
+__global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) / NT)
+    checker_sweep_kernel(CheckerArgs a) {
   constexpr int NWARP = NT / 32;
   // tail items (word j, 4-site group g) packed as bit 8j+g
   using ItmT = typename std::conditional<(WPT <= 4), uint32_t, uint64_t>::type;

@@ -71,9 +71,18 @@ def reduce_best(local_cut, local_bits, first_index: int, num_trials: int, group=
     dev = local_cut.device
     nbytes = local_bits.shape[1]
     if local_cut.numel():
-        idx = torch.arange(first_index, first_index + local_cut.numel(), device=dev,
-                           dtype=torch.int64)
-        keys = (local_cut.to(torch.int64) << 32) | (0xFFFFFFFF - idx)
+        if local_cut.is_cuda:  # key kernel of the library (gsb_best_key)
+            from paper_2505_18508_b200 import _lib
+
+            keys = torch.empty(local_cut.numel(), dtype=torch.int64, device=dev)
+            cut64 = local_cut.to(torch.int64).contiguous()
+            _lib.check(_lib.lib().gsb_best_key(cut64.data_ptr(), cut64.numel(), first_index,
+                                               keys.data_ptr(),
+                                               torch.cuda.current_stream(dev).cuda_stream))
+        else:
+            idx = torch.arange(first_index, first_index + local_cut.numel(), device=dev,
+                               dtype=torch.int64)
+            keys = (local_cut.to(torch.int64) << 32) | (0xFFFFFFFF - idx)
         k = keys.max().reshape(1)
     else:
         k = torch.full((1,), torch.iinfo(torch.int64).min, device=dev, dtype=torch.int64)
