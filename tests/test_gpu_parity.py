@@ -230,3 +230,88 @@ def test_reference_engine_config1_all_trials():
     for i, r in enumerate(rows):
         assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
             r["best_cut"], r["sweeps_executed"], r["hex"]), r["index"]
+
+
+def test_edge_cases_reference_engine(oracle):
+    """Odd n (buffered next32 half), 3xN tori, seed 0 / 2^64-1, one sweep, T = 0."""
+    for (R, C, s) in [(3, 3, 1), (3, 5, 2), (5, 7, 3), (7, 9, 4), (3, 64, 5)]:
+        inst = generate_torus(TorusSpec(R, C, s))
+        eu, ev, ew = oracle.torus_edges(R, C, inst.torus_weights)
+        seeds = [0, 1, 2**63, 2**64 - 1, mix_seed(MASTER, 7)]
+        for cfg in (default_config(ANNEALING, 1, 0), default_config(ANNEALING, 13, 0),
+                    SolverConfig(ANNEALING, 9, 0, 10.0, 9.9), SolverConfig(ANNEALING, 9, 0, 0.5, 1e-3),
+                    default_config(GREEDY, 1, 0), default_config(GREEDY, 50, 0)):
+            b = run_trials(inst, cfg, seeds)
+            bc, bs, se = oracle.run_trials_ref(R * C, eu, ev, ew, cfg.kind, cfg.sweeps, seeds,
+                                               cfg.temp_start, cfg.temp_end)
+            for i in range(len(seeds)):
+                assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+                    bc[i], se[i], oracle.encode_hex(bs[i])), (R, C, cfg, i)
+    b = run_trials(generate_torus(TorusSpec(4, 4, 1)), default_config(ANNEALING, 5, 0), [])
+    assert len(b) == 0
+
+
+def test_randomized_checkerboard_vs_oracle(oracle):
+    """Random even tori, schedules and seeds (both checkerboard engines)."""
+    from paper_2505_18508_b200 import _lib
+
+    rng = np.random.default_rng(2024)
+    for _ in range(12):
+        R = int(rng.integers(2, 12)) * 2
+        C = int(rng.integers(2, 60)) * 2
+        s = int(rng.integers(0, 2**63))
+        t0 = float(rng.uniform(0.5, 5.0))
+        t1 = float(t0 * rng.uniform(0.005, 0.9))
+        S = int(rng.integers(1, 30))
+        inst = generate_torus(TorusSpec(R, C, s))
+        seeds = [int(x) for x in rng.integers(0, 2**63, size=5)] + [0, 2**64 - 1]
+        for kind in (ANNEALING_CHECKERBOARD, GREEDY_CHECKERBOARD):
+            cfg = (SolverConfig(kind, S, 0, t0, t1) if kind == ANNEALING_CHECKERBOARD
+                   else SolverConfig(kind, S, 0))
+            bc, bs, se = oracle.run_trials_checker(R, C, inst.torus_weights, kind, S, seeds,
+                                                   cfg.temp_start, cfg.temp_end)
+            for eng in (None, _lib.ENGINE_CHECKERBOARD_TILED):
+                b = run_trials(inst, cfg, seeds, engine=eng)
+                for i in range(len(seeds)):
+                    assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+                        bc[i], se[i], oracle.encode_hex(bs[i])), (R, C, kind, eng, i)
+
+
+def test_randomized_reference_engine_vs_oracle(oracle):
+    rng = np.random.default_rng(7)
+    for _ in range(10):
+        R, C = int(rng.integers(3, 30)), int(rng.integers(3, 40))
+        inst = generate_torus(TorusSpec(R, C, int(rng.integers(0, 1000))))
+        eu, ev, ew = oracle.torus_edges(R, C, inst.torus_weights)
+        seeds = [int(x) for x in rng.integers(0, 2**63, size=6)]
+        S = int(rng.integers(1, 25))
+        cfg = SolverConfig(ANNEALING, S, 0, float(rng.uniform(0.3, 4)), 0.02)
+        b = run_trials(inst, cfg, seeds)
+        bc, bs, se = oracle.run_trials_ref(R * C, eu, ev, ew, ANNEALING, S, seeds, cfg.temp_start,
+                                           cfg.temp_end)
+        for i in range(len(seeds)):
+            assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+                bc[i], se[i], oracle.encode_hex(bs[i])), (R, C, i)
+
+
+@pytest.mark.parametrize("t0,t1", [(1e12, 1e11), (1e-2, 1e-3), (3.0, 1e-3)])
+def test_threshold_extremes(oracle, t0, t1):
+    """K >= 2^32 (always accept, no draw) and K == 0 (exp underflow) paths."""
+    from paper_2505_18508_b200 import _lib
+
+    inst = generate_torus(TorusSpec(8, 12, 3))
+    seeds = [int(x) for x in mix_seeds(MASTER, range(5))]
+    for kind in (ANNEALING, ANNEALING_CHECKERBOARD):
+        cfg = SolverConfig(kind, 11, 0, t0, t1)
+        if kind == ANNEALING:
+            eu, ev, ew = oracle.torus_edges(8, 12, inst.torus_weights)
+            ref = oracle.run_trials_ref(96, eu, ev, ew, kind, 11, seeds, t0, t1)
+            engines = (None,)
+        else:
+            ref = oracle.run_trials_checker(8, 12, inst.torus_weights, kind, 11, seeds, t0, t1)
+            engines = (None, _lib.ENGINE_CHECKERBOARD_TILED)
+        for eng in engines:
+            b = run_trials(inst, cfg, seeds, engine=eng)
+            for i in range(len(seeds)):
+                assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+                    ref[0][i], ref[2][i], oracle.encode_hex(ref[1][i])), (kind, eng, i)
