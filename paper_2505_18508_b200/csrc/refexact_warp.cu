@@ -41,6 +41,7 @@ struct RefWarpArgs {
   const int8_t *w;        // [2n] torus couplings
   const uint64_t *table;  // [S][4] K = ceil(exp(-d/T)*2^53)
   int sweeps, sa;
+  uint32_t inv_cols;  // ceil(2^32 / cols)
   const uint64_t *seeds;
   int T;
   const uint64_t *jump;  // [33][4] u64: A_k (lo, hi), S_k (lo, hi), k = 1..32 at index k
@@ -228,7 +229,8 @@ __global__ void __launch_bounds__(32) ref_warp_kernel(RefWarpArgs a) {
         int xr = 0, xd = 0, xl = 0, xu = 0;
         if (inb) {
           x = perm[k0 + lane];
-          const int r = x / cols, c = x - r * cols;
+          // x < 2^16: __umulhi with ceil(2^32/cols) is the exact quotient
+          const int r = (int)__umulhi((unsigned)x, a.inv_cols), c = x - r * cols;
           xr = r * cols + (c + 1 == cols ? 0 : c + 1);
           xl = r * cols + (c == 0 ? cols - 1 : c - 1);
           xd = (r + 1 == rows ? 0 : r + 1) * cols + c;
@@ -380,6 +382,7 @@ int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.sweeps_exec = sweeps_exec;
   a.best_bits = best_bits;
   a.nbytes = (n + 7) / 8;
+  a.inv_cols = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)cols - 1) / (uint64_t)cols);
   a.err = err_ws;
   const size_t smem = ref_warp_smem(n);
   if (smem > 48 * 1024 &&
