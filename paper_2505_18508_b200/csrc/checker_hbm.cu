@@ -45,7 +45,8 @@ struct HbmArgs {
   uint32_t *state;  // [T][2][nw]
   uint32_t *best;   // [T][2][nw]
   uint32_t *flips;  // [T][nw] accepted mask of the current half-sweep
-  int *part;        // [2][T][G][2] per-CTA (dsum, psum)
+  int *part;        // [2][T][G] per-CTA Delta sums (tile prefixes)
+  int *acc;         // [3][T][2] per-trial (Delta sum, positive-Delta sum) accumulators
   int *cutp;        // [2][T][G] per-CTA cut partials (init / guard)
   long long *keys;  // [2][T]
   int64_t *best_cut;
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
   uint4 *mk = (uint4 *)smem_raw;  // [2][tw]
   uint4 *gg = mk + 2 * tw;        // [tw]
   int *wsc = (int *)(gg + tw);    // [tw] per-word scratch for the exact search
+  int *isum = wsc + tw;           // [T][tw] (Delta sum << 16) | positive-Delta sum, this phase
 
   for (int i = tid; i < tw; i += HBM_NT) {
     mk[i] = a.masks[w0 + i];
@@ -115,7 +117,10 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
     }
   }
   if (tid == 0 && c == 0)
-    for (int tr = 0; tr < T; tr++) a.keys[tr] = a.keys[T + tr] = LLONG_MIN;
+    for (int tr = 0; tr < T; tr++) {
+      a.keys[tr] = a.keys[T + tr] = LLONG_MIN;
+      for (int buf = 0; buf < 3; buf++) a.acc[(buf * T + tr) * 2] = a.acc[(buf * T + tr) * 2 + 1] = 0;
+    }
   grid.sync();
 
   // ---- initial cut: colour-0 words, partials per CTA
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
   __syncthreads();
 
   unsigned long long tail_blocks = 0;
-  int phase = 0;
+  int phase = 0, hs = 0;  // phase parity, half-sweep counter
   for (int t = 0; t < a.sweeps; t++) {
     uint32_t K2 = 0, K4 = 0;
     bool all2 = false, all4 = false;
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
     const uint32_t K2lo = K2 & 0xFFFFFFu, K4lo = K4 & 0xFFFFFFu;
     if (tid < T) sh.flipped[tid] = 0;
 #pragma unroll 1
-    for (int p = 0; p < 2; p++, phase ^= 1) {
+    for (int p = 0; p < 2; p++, phase ^= 1, hs++) {
       if (tid < T) {
         sh.sd[tid] = 0;
         sh.sp[tid] = 0;
@@ -288,55 +293,58 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
         if (act) {
           __stcg(a.state + ((size_t)tr * 2 + p) * nw + w, Sw ^ A);
           __stcg(a.flips + (size_t)tr * nw + w, A);
+          isum[tr * tw + wl] = (int)((unsigned)wsum << 16) | (wpos & 0xFFFF);
           atomicAdd(&sh.sd[tr], wsum);
           atomicAdd(&sh.sp[tr], wpos);
         }
       }
       __syncthreads();
-      int *pp = a.part + (size_t)phase * T * G * 2;
+      // per-trial totals through global accumulators, triple-buffered by
+      // half-sweep: buffer hs%3 is added to before the barrier, read after it,
+      // and reset one half-sweep later (when every CTA has read it)
+      int *pp = a.part + (size_t)phase * T * G;  // per-CTA Delta sums (prefixes)
+      int *acc = a.acc + (size_t)(hs % 3) * T * 2;
       if (tid < T) {
-        pp[((size_t)tid * G + c) * 2] = sh.sd[tid];
-        pp[((size_t)tid * G + c) * 2 + 1] = sh.sp[tid];
+        pp[(size_t)tid * G + c] = sh.sd[tid];
+        atomicAdd(&acc[2 * tid], sh.sd[tid]);
+        atomicAdd(&acc[2 * tid + 1], sh.sp[tid]);
       }
       grid.sync();
-      // ---- reduce the partials of every trial (every CTA, redundantly)
       if (tid < T) {
-        int D = 0, Pt = 0, pre = 0;
-        for (int i = 0; i < G; i++) {
-          const int d = __ldcg(pp + ((size_t)tid * G + i) * 2);
-          if (i < c) pre += d;
-          D += d;
-          Pt += __ldcg(pp + ((size_t)tid * G + i) * 2 + 1);
-        }
+        const int D = __ldcg(&acc[2 * tid]), Pt = __ldcg(&acc[2 * tid + 1]);
         sh.sd[tid] = D;
-        sh.sp[tid] = pre;  // exclusive prefix of this CTA's tile in id order
+        sh.sp[tid] = 0;
         if (Pt > 0) sh.flipped[tid] = 1;
         sh.scan_need[tid] = sh.active[tid] && (sh.cur[tid] + Pt > sh.bestv[tid]);
-        // reset the key slot of the other parity (its readers are all past this barrier)
-        if (c == 0) a.keys[(phase ^ 1) * T + tid] = LLONG_MIN;
+        if (c == 0) {
+          // the key slot of the other parity and the previous accumulators
+          // have no readers left (all CTAs are past this barrier)
+          a.keys[(phase ^ 1) * T + tid] = LLONG_MIN;
+          int *prev = a.acc + (size_t)((hs + 2) % 3) * T * 2;
+          prev[2 * tid] = 0;
+          prev[2 * tid + 1] = 0;
+        }
       }
       __syncthreads();
       int need = 0;
       for (int tr = 0; tr < T; tr++) need |= sh.scan_need[tr];
       if (need) {
+        // exclusive prefix of this CTA's tile in id order, per trial that needs it
+        for (int tr = 0; tr < T; tr++) {
+          if (!sh.scan_need[tr]) continue;
+          int s = 0;
+          for (int i = tid; i < c; i += HBM_NT) s += __ldcg(pp + (size_t)tr * G + i);
+          s = (int)__reduce_add_sync(0xffffffffu, (unsigned)s);
+          if (lane == 0 && s) atomicAdd(&sh.sp[tr], s);
+        }
+        __syncthreads();
         // ---- exact new-best search for the trials that need it
         for (int tr = 0; tr < T; tr++) {
           if (!sh.scan_need[tr]) continue;
           const uint32_t *cw = a.state + ((size_t)tr * 2 + p) * nw;
           const uint32_t *o = a.state + ((size_t)tr * 2 + (p ^ 1)) * nw;
-          // per-word (sum, first max-prefix) of the pre-phase word in this tile
-          for (int wl = tid; wl < tw; wl += HBM_NT) {
-            const int w = w0 + wl;
-            const uint4 g = gg[wl];
-            const uint32_t A = __ldcg(a.flips + (size_t)tr * nw + w);
-            const uint32_t same = ldcg(o + w);
-            const uint32_t shv = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
-                                            p ? (g.z >> 16) : (g.z & 0xFFFFu));
-            const Classes cl = classes(ldcg(cw + w) ^ A, same, shv, ldcg(o + (g.x & 0xFFFFu)),
-                                       ldcg(o + (g.x >> 16)), mk[p * tw + wl], g.w);
-            wsc[wl] = 2 * __popc(A & cl.k3) + 4 * __popc(A & cl.k4) - 2 * __popc(A & cl.km2) -
-                      4 * __popc(A & cl.km4);
-          }
+          // per-word Delta sums of this half-sweep, recorded by the main pass
+          for (int wl = tid; wl < tw; wl += HBM_NT) wsc[wl] = isum[tr * tw + wl] >> 16;
           __syncthreads();
           // exclusive scan of wsc over the tile (warp 0, chunked)
           if (warp == 0) {
@@ -362,6 +370,9 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
           const int base = sh.cur[tr] + sh.sp[tr];
           for (int wl = tid; wl < tw; wl += HBM_NT) {
             const int w = w0 + wl;
+            // only words whose positive-Delta bound can beat best are candidates
+            const int pos_bound0 = isum[tr * tw + wl] & 0xFFFF;
+            if (pos_bound0 == 0 || base + wsc[wl] + pos_bound0 <= sh.bestv[tr]) continue;
             const uint4 g = gg[wl];
             const uint32_t A = __ldcg(a.flips + (size_t)tr * nw + w);
             if (!A) continue;
@@ -503,7 +514,7 @@ size_t checker_hbm_workspace_bytes(int rows, int cols, int T, int nsm) {
   b += 2 * align_up((size_t)TB * 2 * nw * 4, 256);                                 // state, best
   b += align_up((size_t)TB * nw * 4, 256);                                         // flips
   b += align_up((size_t)2 * TB * G * 2 * 4, 256) + align_up((size_t)2 * TB * G * 4, 256);
-  b += align_up((size_t)2 * TB * 8, 256);
+  b += align_up((size_t)2 * TB * 8, 256) + align_up((size_t)3 * TB * 2 * 4, 256);  // keys, acc
   return b;
 }
 
@@ -544,7 +555,7 @@ int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweep
   for (int per = 4; per >= 1; per--) {
     const int g = nsm * per;
     const int tw = (nw + g - 1) / g;
-    const size_t s = (size_t)tw * 16 * 3 + (size_t)tw * 4 + 16;
+    const size_t s = (size_t)tw * 16 * 3 + (size_t)tw * 4 * (1 + HBM_MAX_T) + 16;
     if (s > 200 * 1024) continue;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s) !=
         cudaSuccess)
@@ -564,6 +575,8 @@ int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweep
   int *cutp = (int *)p;
   p += align_up((size_t)2 * TB * G * 4, 256);
   long long *keys = (long long *)p;
+  p += align_up((size_t)2 * TB * 8, 256);
+  int *acc = (int *)p;
 
   for (int t0 = 0; t0 < T; t0 += HBM_MAX_T) {
     HbmArgs a;
@@ -582,6 +595,7 @@ int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweep
     a.best = best;
     a.flips = flips;
     a.part = part;
+    a.acc = acc;
     a.cutp = cutp;
     a.keys = keys;
     a.best_cut = best_cut + t0;

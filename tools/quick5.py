@@ -4,7 +4,7 @@ from paper_2505_18508_b200 import TorusSpec, generate_torus
 from paper_2505_18508_b200.campaign import mix_seeds
 from paper_2505_18508_b200.solvers import *
 inst = generate_torus(TorusSpec(2000, 2000, 1))
-for T, S in [(8, 20), (8, 100)]:
+for T, S in [(8, 100), (8, 1000)]:
     cfg = default_config(ANNEALING_CHECKERBOARD, S, 0)
     seeds = mix_seeds(20250814, range(T))
     run_trials_device(inst, cfg, seeds); torch.cuda.synchronize()
