@@ -205,10 +205,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # development only: GSB_BENCH_SHARE_GPU=1 puts every rank on cuda:0 and uses
+    # gloo, to exercise the torchrun path on a one-GPU box (ranks never wait on
+    # each other inside a kernel); production runs use one GPU per rank + NCCL
+    share = os.environ.get("GSB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     rows, cols, T, S = CONFIGS[a.config]
     T = a.trials or T
