@@ -17,8 +17,8 @@
 // (4 sign planes per word, uint4) and the best-so-far snapshot.
 //
 // Per word and half-sweep: 4 positive-term planes P_j = ~(S^N_j^NEG_j),
-// bit-sliced counts -> Delta classes, then for the Delta<0 sites an MSB-first
-// bit-sliced comparison of the 32-bit uniform with K = ceil(exp(Delta/T)*2^32):
+// bit-sliced counts -> Delta classes, then for the Delta<0 sites a bit-sliced
+// comparison (borrow chain) of the 32-bit uniform with K = ceil(exp(Delta/T)*2^32):
 // uniform bits 31..24 are 8 Philox planes (two calls per word, unconditional);
 // sites still undecided after them take bits 23..0 from a per-site Philox word
 // (contract v2), drawn for the whole warp in one cooperative round.
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
   int *red2 = red + 4 * NWARP;                    // [2][NWARP]
   int *scan = red2 + 2 * NWARP;                   // [WPT][NWARP]
   long long *kred = (long long *)(scan + ((WPT * NWARP + 1) & ~1));  // [NWARP]
-  int *wctrs = (int *)(kred + NWARP);              // [NWARP] tail slot counters
+  unsigned *wctrs = (unsigned *)(kred + NWARP);    // [NWARP] tail slot counters
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
   uint32_t *tc2 = teq + WPT * 32;            // [WPT][32] class -2 masks
   uint32_t *tlt = tc2 + WPT * 32;            // [WPT][32] accepted-by-tail bits
   uint32_t *myq = tq + warp * 32;
-  int *wctr = wctrs + warp;
+  unsigned *wctr = wctrs + warp;
 
   for (int i = tid; i < 2 * nw; i += NT) msk[i] = a.masks[i];
   for (int i = tid; i < nw; i += NT) geo[i] = a.geo[i];
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
 
   bool own[WPT];
 #pragma unroll
-  for (int j = 0; j < WPT; j++) own[j] = j * NT + tid < nw;
+  for (int j = 0; j < WPT; j++) own[j] = j < WPT - 1 || j * NT + tid < nw;  // WPT = ceil(nw/NT)
 
   unsigned tail_blocks = 0;
   for (int trial = blockIdx.x; trial < a.T; trial += gridDim.x) {
@@ -231,14 +231,15 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
         const uint32_t *o = st + (p ^ 1) * nw;
         uint32_t A[WPT], c2[WPT], eq[WPT], lt[WPT];
         int wpos[WPT], wsum[WPT];
-        ItmT itm = 0;
-        // ---- pass 1: classes and the unconditional planes 0-7
+        // ---- pass 1: classes and the unconditional planes 0-7.  Words j <
+        // WPT-1 are owned by every lane (the launch picks WPT = ceil(nw/NT)),
+        // so only the last one is guarded and the bodies schedule together.
 #pragma unroll
         for (int j = 0; j < WPT; j++) {
           const int wi = j * NT + tid;
           A[j] = c2[j] = eq[j] = lt[j] = 0;
           wpos[j] = wsum[j] = 0;
-          if (own[j]) {
+          if (j < WPT - 1 || own[j]) {
             const uint4 g = geo[wi];
             const uint4 m = msk[p * nw + wi];
             const uint32_t same = oth_w[j];
@@ -262,26 +263,22 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
               const uint32_t e2 = (all2 || K2 == 0) ? 0u : c.km2;
               const uint32_t e4 = (all4 || K4 == 0) ? 0u : c.km4;
               c2[j] = e2;
-              uint32_t q = e2 | e4, l = 0;
+              const uint32_t pend = e2 | e4;
+              uint32_t q = pend, l = 0;
               const P4 r0 =
                   philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p), 1u}, key0, key1);
               const P4 r1 =
                   philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p + 1), 1u}, key0, key1);
-              cmp_plane(r0.x, e2, ma[0], mb[0], q, l);
-              cmp_plane(r0.y, e2, ma[1], mb[1], q, l);
-              cmp_plane(r0.z, e2, ma[2], mb[2], q, l);
-              cmp_plane(r0.w, e2, ma[3], mb[3], q, l);
-              cmp_plane(r1.x, e2, ma[4], mb[4], q, l);
-              cmp_plane(r1.y, e2, ma[5], mb[5], q, l);
-              cmp_plane(r1.z, e2, ma[6], mb[6], q, l);
-              cmp_plane(r1.w, e2, ma[7], mb[7], q, l);
+              cmp_plane_lsb(r1.w, e2, ma[7], mb[7], q, l);
+              cmp_plane_lsb(r1.z, e2, ma[6], mb[6], q, l);
+              cmp_plane_lsb(r1.y, e2, ma[5], mb[5], q, l);
+              cmp_plane_lsb(r1.x, e2, ma[4], mb[4], q, l);
+              cmp_plane_lsb(r0.w, e2, ma[3], mb[3], q, l);
+              cmp_plane_lsb(r0.z, e2, ma[2], mb[2], q, l);
+              cmp_plane_lsb(r0.y, e2, ma[1], mb[1], q, l);
+              cmp_plane_lsb(r0.x, e2, ma[0], mb[0], q, l);
               eq[j] = q;
-              lt[j] = l;
-              if (q) {
-                teq[j * 32 + lane] = q;
-                tc2[j * 32 + lane] = e2;
-                itm |= (ItmT)nibmask8(q) << (8 * j);
-              }
+              lt[j] = l & pend;
             } else {
               A[j] = c.k3 | c.k4;
               wsum[j] = wpos[j];
@@ -292,16 +289,27 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
         // 23..0 of their uniform from a per-site Philox word; the warp draws
         // all pending 4-site groups together, 32 per round.
         if (SA) {
-          bool any_tail = false;
+          uint32_t anyq = 0;
+#pragma unroll
+          for (int j = 0; j < WPT; j++) anyq |= eq[j];
+          if (__any_sync(0xffffffffu, anyq != 0u)) {
+          ItmT itm = 0;
+#pragma unroll
+          for (int j = 0; j < WPT; j++) {
+            teq[j * 32 + lane] = eq[j];
+            tc2[j * 32 + lane] = c2[j];
+            itm |= (ItmT)nibmask8(eq[j]) << (8 * j);
+          }
+          // slots come from a per-warp counter that only grows (wbase = its
+          // value when this tail started); the total from one REDUX
+          const unsigned wbase = *wctr;
 #pragma unroll 1
-          while (true) {
+          for (unsigned done = 0;;) {
             const int cnt = popc_itm(itm);
-            const int sbase = cnt ? atomicAdd(wctr, cnt) : 0;
-            __syncwarp();
-            const int total = *wctr;
+            const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
             if (total == 0) break;
+            const int sbase = (int)((cnt ? atomicAdd(wctr, (unsigned)cnt) : 0u) - wbase - done);
             tail_blocks += (unsigned)min(total, 32);
-            any_tail = true;
             int slot = sbase;
             while (itm && slot < 32) {
               const int bpos = ffs_itm(itm) - 1;
@@ -326,17 +334,15 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
               if (ln) atomicOr(&tlt[jj * 32 + ol], ln << (4 * gi));
             }
             __syncwarp();
-            if (lane == 0) *wctr = 0;
-            __syncwarp();
+            done += (unsigned)total;
           }
-          if (any_tail) {
 #pragma unroll
-            for (int j = 0; j < WPT; j++) {
-              if (eq[j]) {
-                lt[j] |= tlt[j * 32 + lane];
-                tlt[j * 32 + lane] = 0;
-              }
+          for (int j = 0; j < WPT; j++) {
+            if (eq[j]) {
+              lt[j] |= tlt[j * 32 + lane];
+              tlt[j * 32 + lane] = 0;
             }
+          }
           }
         }
         // ---- pass 3: commit the flips
@@ -642,24 +648,32 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.err = err_ws;
   a.blocks = (unsigned long long *)((char *)err_ws + 8);
   const bool sa = kind == GSB_ANNEALING;
-  // Team shape: W warps per trial (power of two), WPT words per lane.  Aim
-  // for >= ~12 resident warps per SM with as few warps per trial as possible
-  // (cheap barriers, more ILP per lane) and WPT <= 6.
+  // Team shape: W warps per trial (power of two), WPT words per lane.  As few
+  // warps per trial as possible: a one-warp team needs no CTA barriers at all
+  // (measured best up to WPT = 8); larger teams keep WPT <= 6.  Grow the team
+  // only while the trials cannot give every SM at least two warps.
   int W = 1;
   while (W < 16 && 32 * W < nw &&
-         ((long long)T * W < 12LL * nsm || (nw + 32 * W - 1) / (32 * W) > 6))
+         ((long long)T * W < 2LL * nsm || (nw + 32 * W - 1) / (32 * W) > (W == 1 ? 8 : 6)))
     W *= 2;
   if (const char *ov = getenv("GSB_CHECKER_WARPS")) {  // development tuning knob
     const int w = atoi(ov);
-    if (w == 1 || w == 2 || w == 4 || w == 8 || w == 16) W = w;
+    if ((w == 1 || w == 2 || w == 4 || w == 8 || w == 16) && (nw + 32 * w - 1) / (32 * w) <= 8)
+      W = w;
   }
   const int wpt = (nw + 32 * W - 1) / (32 * W);
-  if (wpt <= 1) return launch_wpt<1>(a, sa, nsm, W, stream);
-  if (wpt <= 2) return launch_wpt<2>(a, sa, nsm, W, stream);
-  if (wpt <= 3) return launch_wpt<3>(a, sa, nsm, W, stream);
-  if (wpt <= 4) return launch_wpt<4>(a, sa, nsm, W, stream);
-  if (wpt <= 6) return launch_wpt<6>(a, sa, nsm, W, stream);
-  return launch_wpt<8>(a, sa, nsm, W, stream);
+  if (wpt > 8) return set_error(GSB_EUNSUPPORTED, "checkerboard team shape out of range");
+  // the kernel relies on WPT == ceil(nw / NT) exactly (all but the last word owned)
+  switch (wpt) {
+    case 1: return launch_wpt<1>(a, sa, nsm, W, stream);
+    case 2: return launch_wpt<2>(a, sa, nsm, W, stream);
+    case 3: return launch_wpt<3>(a, sa, nsm, W, stream);
+    case 4: return launch_wpt<4>(a, sa, nsm, W, stream);
+    case 5: return launch_wpt<5>(a, sa, nsm, W, stream);
+    case 6: return launch_wpt<6>(a, sa, nsm, W, stream);
+    case 7: return launch_wpt<7>(a, sa, nsm, W, stream);
+    default: return launch_wpt<8>(a, sa, nsm, W, stream);
+  }
 }
 
 }  // namespace gsb

@@ -54,13 +54,16 @@ __device__ __forceinline__ Classes classes(uint32_t Sw, uint32_t same, uint32_t 
   return c;
 }
 
-// MSB-first bit-sliced compare step for one plane.  c2 = class -2 sites
-// (threshold K2), other pending sites use K4; ma/mb = all-ones iff the
-// plane's bit of K2/K4 is set (per sweep, uniform).  4 LOP3 per plane.
-__device__ __forceinline__ void cmp_plane(uint32_t R, uint32_t c2, uint32_t ma, uint32_t mb,
-                                          uint32_t &eq, uint32_t &lt) {
+// Bit-sliced comparison of the uniforms' top 8 bits with the thresholds, as a
+// borrow chain over the planes LSB-first (plane 7 = uniform bit 24 first,
+// plane 0 = bit 31 last).  c2 = class -2 sites (threshold K2), other pending
+// sites use K4; ma/mb = all-ones iff the plane's bit of K2/K4 is set (per
+// sweep, uniform).  lt becomes [u_hi < K_hi] (strict), eq keeps the pending
+// sites whose 8 bits all equal K_hi.  3 LOP3 per plane.
+__device__ __forceinline__ void cmp_plane_lsb(uint32_t R, uint32_t c2, uint32_t ma, uint32_t mb,
+                                              uint32_t &eq, uint32_t &lt) {
   const uint32_t tb = (c2 & ma) | (~c2 & mb);
-  lt |= eq & ~R & tb;
+  lt = (tb & (~R | lt)) | (~tb & ~R & lt);
   eq &= ~(R ^ tb);
 }
 

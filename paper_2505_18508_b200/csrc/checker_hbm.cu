@@ -215,20 +215,21 @@ __global__ void __launch_bounds__(HBM_NT) checker_hbm_kernel(HbmArgs a) {
             const uint32_t e2 = (all2 || K2 == 0) ? 0u : cl.km2;
             const uint32_t e4 = (all4 || K4 == 0) ? 0u : cl.km4;
             c2 = e2;
-            uint32_t q = e2 | e4, l = 0;
+            const uint32_t pend = e2 | e4;
+            uint32_t q = pend, l = 0;
             const P4 r0 = philox10(P4{(uint32_t)w, (uint32_t)t, (uint32_t)(2 * p), 1u}, key0, key1);
             const P4 r1 =
                 philox10(P4{(uint32_t)w, (uint32_t)t, (uint32_t)(2 * p + 1), 1u}, key0, key1);
-            cmp_plane(r0.x, e2, ma[0], mb[0], q, l);
-            cmp_plane(r0.y, e2, ma[1], mb[1], q, l);
-            cmp_plane(r0.z, e2, ma[2], mb[2], q, l);
-            cmp_plane(r0.w, e2, ma[3], mb[3], q, l);
-            cmp_plane(r1.x, e2, ma[4], mb[4], q, l);
-            cmp_plane(r1.y, e2, ma[5], mb[5], q, l);
-            cmp_plane(r1.z, e2, ma[6], mb[6], q, l);
-            cmp_plane(r1.w, e2, ma[7], mb[7], q, l);
+            cmp_plane_lsb(r1.w, e2, ma[7], mb[7], q, l);
+            cmp_plane_lsb(r1.z, e2, ma[6], mb[6], q, l);
+            cmp_plane_lsb(r1.y, e2, ma[5], mb[5], q, l);
+            cmp_plane_lsb(r1.x, e2, ma[4], mb[4], q, l);
+            cmp_plane_lsb(r0.w, e2, ma[3], mb[3], q, l);
+            cmp_plane_lsb(r0.z, e2, ma[2], mb[2], q, l);
+            cmp_plane_lsb(r0.y, e2, ma[1], mb[1], q, l);
+            cmp_plane_lsb(r0.x, e2, ma[0], mb[0], q, l);
             eq = q;
-            lt = l;
+            lt = l & pend;
             tail_blocks += 2;
           } else {
             A = cl.k3 | cl.k4;
