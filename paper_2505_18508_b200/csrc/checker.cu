@@ -113,21 +113,14 @@ struct CheckerArgs {
   unsigned long long *blocks;  // Philox blocks drawn (statistics, workspace)
 };
 
-__device__ __forceinline__ int popc_itm(uint32_t x) { return __popc(x); }
-__device__ __forceinline__ int popc_itm(uint64_t x) { return __popcll(x); }
-__device__ __forceinline__ int ffs_itm(uint32_t x) { return __ffs(x); }
-__device__ __forceinline__ int ffs_itm(uint64_t x) { return __ffsll((long long)x); }
 
-template <int NT, int WPT, bool SA>
-#ifndef GSB_CHECKER_WARPS_PER_SM
-#define GSB_CHECKER_WARPS_PER_SM 16
-#endif
-__global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) / NT)
-    checker_sweep_kernel(CheckerArgs a) {
+// MINB = resident CTAs per SM the register budget is cut for: 16 warps per
+// SM by default, 8 for one-warp teams whose trials cannot fill more (twice
+// the registers per lane for interleaving the word bodies).
+template <int NT, int WPT, bool SA, int MINB>
+__global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) {
   constexpr int NWARP = NT / 32;
-  // tail items (word j, 4-site group g) packed as bit 8j+g
-  using ItmT = typename std::conditional<(WPT <= 4), uint32_t, uint64_t>::type;
-  static_assert(WPT <= 8, "tail item index packs 8 words x 8 groups");
+  static_assert(WPT <= 8, "tail items pack (lane, word) as lane << 3 | j");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = a.nw;
   uint4 *msk = (uint4 *)smem_raw;                 // [2][nw]
@@ -286,63 +279,69 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
           }
         }
         // ---- pass 2 (SA): warp-cooperative tail.  Undecided sites take bits
-        // 23..0 of their uniform from a per-site Philox word; the warp draws
-        // all pending 4-site groups together, 32 per round.
+        // 23..0 of their uniform from a per-site Philox word; the warp shares
+        // out the words that hold undecided sites (items), 32 per round, and
+        // each item walks its 4-site groups (one Philox block per group).
         if (SA) {
-          uint32_t anyq = 0;
+          uint32_t wm = 0;  // bit j: word j has undecided sites
 #pragma unroll
-          for (int j = 0; j < WPT; j++) anyq |= eq[j];
-          if (__any_sync(0xffffffffu, anyq != 0u)) {
-          ItmT itm = 0;
+          for (int j = 0; j < WPT; j++) wm |= (eq[j] != 0u ? 1u : 0u) << j;
+          if (__any_sync(0xffffffffu, wm != 0u)) {
 #pragma unroll
-          for (int j = 0; j < WPT; j++) {
-            teq[j * 32 + lane] = eq[j];
-            tc2[j * 32 + lane] = c2[j];
-            itm |= (ItmT)nibmask8(eq[j]) << (8 * j);
-          }
-          // slots come from a per-warp counter that only grows (wbase = its
-          // value when this tail started); the total from one REDUX
-          const unsigned wbase = *wctr;
-#pragma unroll 1
-          for (unsigned done = 0;;) {
-            const int cnt = popc_itm(itm);
-            const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
-            if (total == 0) break;
-            const int sbase = (int)((cnt ? atomicAdd(wctr, (unsigned)cnt) : 0u) - wbase - done);
-            tail_blocks += (unsigned)min(total, 32);
-            int slot = sbase;
-            while (itm && slot < 32) {
-              const int bpos = ffs_itm(itm) - 1;
-              itm &= itm - 1;
-              myq[slot++] = ((uint32_t)lane << 8) | (uint32_t)bpos;
-            }
-            __syncwarp();
-            if (lane < total) {
-              const uint32_t it = myq[lane];
-              const int ol = (int)(it >> 8), jj = (int)((it >> 3) & 7u), gi = (int)(it & 7u);
-              const uint32_t wi = (uint32_t)(jj * NT + warp * 32 + ol);
-              const P4 r = philox10(P4{wi, (uint32_t)t, (uint32_t)(4 + 8 * p + gi), 1u}, key0, key1);
-              const uint32_t en = (teq[jj * 32 + ol] >> (4 * gi)) & 0xFu;
-              const uint32_t cn = (tc2[jj * 32 + ol] >> (4 * gi)) & 0xFu;
-              const uint32_t tw[4] = {r.x, r.y, r.z, r.w};
-              uint32_t ln = 0;
-#pragma unroll
-              for (int q = 0; q < 4; q++) {
-                const uint32_t klo = ((cn >> q) & 1u) ? K2lo : K4lo;
-                if (((en >> q) & 1u) && (tw[q] >> 8) < klo) ln |= 1u << q;
+            for (int j = 0; j < WPT; j++) {
+              if (eq[j]) {
+                teq[j * 32 + lane] = eq[j];
+                tc2[j * 32 + lane] = c2[j];
               }
-              if (ln) atomicOr(&tlt[jj * 32 + ol], ln << (4 * gi));
             }
-            __syncwarp();
-            done += (unsigned)total;
-          }
+            // slots come from a per-warp counter that only grows (wbase = its
+            // value when this tail started); the total from one REDUX
+            const unsigned wbase = *wctr;
+            uint32_t rem = wm;
+#pragma unroll 1
+            for (unsigned done = 0;;) {
+              const int cnt = __popc(rem);
+              const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+              if (total == 0) break;
+              const int sbase = (int)((cnt ? atomicAdd(wctr, (unsigned)cnt) : 0u) - wbase - done);
+              int slot = sbase;
+              while (rem && slot < 32) {
+                const int jj = __ffs(rem) - 1;
+                rem &= rem - 1;
+                myq[slot++] = ((uint32_t)lane << 3) | (uint32_t)jj;
+              }
+              __syncwarp();
+              if (lane < total) {
+                const uint32_t it = myq[lane];
+                const int ol = (int)(it >> 3), jj = (int)(it & 7u);
+                const uint32_t wi = (uint32_t)(jj * NT + warp * 32 + ol);
+                uint32_t e = teq[jj * 32 + ol];
+                const uint32_t cw = tc2[jj * 32 + ol];
+                uint32_t acc = 0;
+                while (e) {
+                  const int g4 = (__ffs(e) - 1) & ~3;  // 4 * group
+                  const P4 r = philox10(P4{wi, (uint32_t)t, (uint32_t)(4 + 8 * p + (g4 >> 2)), 1u},
+                                        key0, key1);
+                  tail_blocks++;
+                  const uint32_t en = (e >> g4) & 0xFu, cn = (cw >> g4) & 0xFu;
+                  const uint32_t tw[4] = {r.x, r.y, r.z, r.w};
+                  uint32_t ln = 0;
 #pragma unroll
-          for (int j = 0; j < WPT; j++) {
-            if (eq[j]) {
-              lt[j] |= tlt[j * 32 + lane];
-              tlt[j * 32 + lane] = 0;
+                  for (int q = 0; q < 4; q++) {
+                    const uint32_t klo = ((cn >> q) & 1u) ? K2lo : K4lo;
+                    if (((en >> q) & 1u) && (tw[q] >> 8) < klo) ln |= 1u << q;
+                  }
+                  acc |= ln << g4;
+                  e &= ~(0xFu << g4);
+                }
+                tlt[jj * 32 + ol] = acc;  // one item per (word, lane): plain store
+              }
+              __syncwarp();
+              done += (unsigned)total;
             }
-          }
+#pragma unroll
+            for (int j = 0; j < WPT; j++)
+              if (eq[j]) lt[j] |= tlt[j * 32 + lane];
           }
         }
         // ---- pass 3: commit the flips
@@ -385,19 +384,32 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
         if (Pt > 0) sweep_flipped = true;  // greedy flips are exactly the positive ones
         if (cur + Pt > best) {
           // ---- per-word prefix bounds; word order is (j, warp, lane)
+          // Two words per scan: wsum + 128 is in [0, 256], so a 32-lane
+          // prefix fits 16 bits (<= 8192) and pairs (j, j+1) share one scan.
           int excl[WPT];
           int rtot[WPT];
 #pragma unroll
-          for (int j = 0; j < WPT; j++) {
-            int incl = wsum[j];
+          for (int j = 0; j < WPT; j += 2) {
+            const bool two = j + 1 < WPT;
+            uint32_t x = (uint32_t)(wsum[j] + 128) |
+                         (two ? (uint32_t)(wsum[two ? j + 1 : j] + 128) << 16 : 0u);
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-              const int y = __shfl_up_sync(0xffffffffu, incl, off);
-              if (lane >= off) incl += y;
+              const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
+              if (lane >= off) x += y;
             }
-            excl[j] = incl - wsum[j];
-            rtot[j] = __shfl_sync(0xffffffffu, incl, 31);
-            if (NWARP > 1 && lane == 31) scan[j * NWARP + warp] = incl;
+            const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+            const int bias = 128 * (lane + 1);
+            excl[j] = (int)(x & 0xFFFFu) - bias - wsum[j];
+            rtot[j] = (int)(tot & 0xFFFFu) - 4096;
+            if (two) {
+              excl[j + 1] = (int)(x >> 16) - bias - wsum[j + 1];
+              rtot[j + 1] = (int)(tot >> 16) - 4096;
+            }
+          }
+          if (NWARP > 1 && lane == 31) {
+#pragma unroll
+            for (int j = 0; j < WPT; j++) scan[j * NWARP + warp] = rtot[j];
           }
           if (NWARP > 1) __syncthreads();
           int basep = 0;
@@ -523,8 +535,7 @@ __global__ void __launch_bounds__(NT, (GSB_CHECKER_WARPS_PER_SM * 32 + NT - 1) /
     {
       // Philox blocks of this trial: 2 init + 2 plane blocks per word and
       // half-sweep (SA) + the cooperative tail groups
-      unsigned long long nb = (unsigned long long)tail_blocks;
-      nb = __reduce_add_sync(0xffffffffu, lane == 0 ? (unsigned)nb : 0u);
+      const unsigned long long nb = __reduce_add_sync(0xffffffffu, tail_blocks);
       if (lane == 0 && nb) atomicAdd(a.blocks, nb);
       if (tid == 0)
         atomicAdd(a.blocks, 2ull * nw + (SA ? 4ull * nw * (unsigned long long)executed : 0ull));
@@ -564,10 +575,11 @@ static size_t smem_bytes(int nw, int NT, int WPT) {
   return b;
 }
 
-template <int NT, int WPT>
+template <int NT, int WPT, int MINB = 512 / NT>
 static int launch_nt(const CheckerArgs &a, bool sa, int nsm, cudaStream_t stream) {
   const size_t smem = smem_bytes(a.nw, NT, WPT);
-  auto kern = sa ? checker_sweep_kernel<NT, WPT, true> : checker_sweep_kernel<NT, WPT, false>;
+  auto kern = sa ? checker_sweep_kernel<NT, WPT, true, MINB>
+                 : checker_sweep_kernel<NT, WPT, false, MINB>;
   if (smem > 48 * 1024) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
@@ -608,7 +620,9 @@ size_t checker_workspace_bytes(int rows, int cols) {
 template <int WPT>
 static int launch_wpt(const CheckerArgs &a, bool sa, int nsm, int W, cudaStream_t stream) {
   switch (W) {
-    case 1: return launch_nt<32, WPT>(a, sa, nsm, stream);
+    case 1:
+      if (a.T <= 8 * nsm && !getenv("GSB_CHECKER_THIN")) return launch_nt<32, WPT, 8>(a, sa, nsm, stream);
+      return launch_nt<32, WPT>(a, sa, nsm, stream);
     case 2: return launch_nt<64, WPT>(a, sa, nsm, stream);
     case 4: return launch_nt<128, WPT>(a, sa, nsm, stream);
     case 8: return launch_nt<256, WPT>(a, sa, nsm, stream);
