@@ -387,8 +387,9 @@ def main():
         "algorithmic_units_per_launch": blocks_per_step,
         "unit_def": "Philox4x32-10 blocks the checkerboard contract requires (2 init + 8 "
                     "planes per word and half-sweep + per-site tail groups), counted by the kernel",
-        "peak_basis": "measured live: gsb_philox_bench, SMs x 8 x 256 threads evaluating "
-                      "independent Philox4x32-10 blocks (uniform key), CUDA events",
+        "peak_basis": "measured live: gsb_philox_bench, SMs x 8 x 256 threads, 2 independent "
+                      "Philox4x32-10 blocks in flight per thread (uniform key; the fastest "
+                      "mix in tools/philox_mb.cu), CUDA events",
         "updates_per_launch": upd_per_step_rank,
         "launch_ms": launch_s * 1e3,
         "updates_per_s": kernel_rate,

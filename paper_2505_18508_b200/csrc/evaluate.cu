@@ -148,16 +148,18 @@ int best_key(const int64_t *best_cut, int T, int64_t first, int64_t *key, cudaSt
 }
 
 // Philox4x32-10 throughput microbenchmark: every thread evaluates
-// `blocks_per_thread` independent blocks (4 streams interleaved for ILP) and
-// XOR-folds the outputs.  Grid = SMs x 8 CTAs x 256 threads.
+// `blocks_per_thread` independent blocks (2 streams interleaved for ILP: the
+// fastest mix in tools/philox_mb.cu) and XOR-folds the outputs.
+// Grid = SMs x 8 CTAs x 256 threads.
 __global__ void __launch_bounds__(256) philox_bench_kernel(int64_t n, uint32_t *sink) {
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t k0 = 0x12345678u ^ blockIdx.x, k1 = 0x9abcdef0u;  // uniform key, as in a trial
   uint32_t acc = 0;
-  for (int64_t i = 0; i < n; i += 4) {
+  const int iters = (int)(n / 2);
+  for (int i = 0; i < iters; i++) {
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const P4 r = philox10(P4{tid, (uint32_t)(i + q), 7u, 1u}, k0, k1);
+    for (int q = 0; q < 2; q++) {
+      const P4 r = philox10(P4{tid, (uint32_t)i, (uint32_t)q, 1u}, k0, k1);
       acc ^= r.x ^ r.y ^ r.z ^ r.w;
     }
   }
