@@ -77,7 +77,9 @@ __global__ void checker_masks_kernel(int rows, int cols, int WPR, const int8_t *
       if (w_up < 0) nu |= 1u << b;
       if (w_down < 0) nd |= 1u << b;
     }
-    masks[idx] = make_uint4(ns, nsh, nu, nd);
+    // padding bits: NU/ND set, NS/NSH clear -> a padding site (spin and
+    // neighbours 0) sees exactly two positive terms (classes_pad)
+    masks[idx] = make_uint4(ns, nsh, nu | ~v, nd | ~v);
     if (p == 0) {
       uint32_t cidx[2], cinfo[2];
       for (int q = 0; q < 2; q++) {
@@ -236,12 +238,12 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
             const uint4 g = geo[wi];
             const uint4 m = msk[p * nw + wi];
             const uint32_t same = oth_w[j];
-            const uint32_t sh = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
-                                           p ? (g.z >> 16) : (g.z & 0xFFFFu));
-            const Classes c = classes(cur_w[j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m, g.w);
+            const uint32_t sh = shifted_nb_v(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
+                                             p ? (g.z >> 16) : (g.z & 0xFFFFu), g.w);
+            const Classes c = classes_pad(cur_w[j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m);
             wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
             if (SA) {
-              uint32_t b = c.ge2;
+              uint32_t b = c.ge2 & g.w;
               int neg = 0;
               if (all2) {
                 b |= c.km2;
@@ -440,10 +442,10 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
               const uint4 g = geo[wi];
               const uint32_t Sold = cur_w[j] ^ A[j];
               const uint32_t same = oth_w[j];
-              const uint32_t sh = shifted_nb(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
-                                             p ? (g.z >> 16) : (g.z & 0xFFFFu));
-              const Classes c = classes(Sold, same, sh, o[g.x & 0xFFFFu], o[g.x >> 16],
-                                        msk[p * nw + wi], g.w);
+              const uint32_t sh = shifted_nb_v(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
+                                               p ? (g.z >> 16) : (g.z & 0xFFFFu), g.w);
+              const Classes c = classes_pad(Sold, same, sh, o[g.x & 0xFFFFu], o[g.x >> 16],
+                                            msk[p * nw + wi]);
               const uint32_t Aj = A[j];
               const uint32_t P2 = Aj & c.k3, P4m = Aj & c.k4, N2 = Aj & c.km2, N4 = Aj & c.km4;
               int v = cur + excl[j], mx = INT_MIN, mp = -1;

@@ -8,6 +8,15 @@
 
 namespace gsb {
 
+// lop3.b32 with an explicit truth table (a = 0xF0, b = 0xCC, c = 0xAA): nvcc
+// splits some 3-input functions into two LOP3s, this keeps them one.
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t shifted_nb(const uint32_t *__restrict__ o, uint32_t same,
                                                uint32_t cidx, uint32_t cinfo) {
   const uint32_t src = cinfo & 31u, dst = (cinfo >> 5) & 31u;
@@ -54,6 +63,39 @@ __device__ __forceinline__ Classes classes(uint32_t Sw, uint32_t same, uint32_t 
   return c;
 }
 
+// Shifted neighbour word with its padding bits cleared (V = valid bits): the
+// input classes_pad() expects.
+__device__ __forceinline__ uint32_t shifted_nb_v(const uint32_t *__restrict__ o, uint32_t same,
+                                                 uint32_t cidx, uint32_t cinfo, uint32_t V) {
+  const uint32_t src = cinfo & 31u, dst = (cinfo >> 5) & 31u;
+  const uint32_t carry = ((o[cidx] >> src) & 1u) << dst;
+  const uint32_t t = ((cinfo >> 10) & 1u) ? (same >> 1) : (same << 1);
+  return lop3<0xA8>(t, carry, V);  // (t | carry) & V
+}
+
+// Delta classes in 11 LOP3s, using the padding convention of
+// checker_masks_kernel (coupling planes NU/ND set, NS/NSH clear on padding
+// bits) and padding-free spin/neighbour words: a padding site then has
+// exactly two positive terms (Delta = 0), so k3/k4/km2/km4 never contain it
+// and only ge2 must be masked with V by the caller.
+//   a+b+c = 2*c1 + s1 (full adder), #positive = 2*c1 + s1 + d
+__device__ __forceinline__ Classes classes_pad(uint32_t Sw, uint32_t same, uint32_t sh, uint32_t up,
+                                               uint32_t dn, uint4 m) {
+  const uint32_t a = lop3<0x69>(Sw, same, m.x);  // ~(x ^ y ^ z)
+  const uint32_t b = lop3<0x69>(Sw, sh, m.y);
+  const uint32_t c = lop3<0x69>(Sw, up, m.z);
+  const uint32_t d = lop3<0x69>(Sw, dn, m.w);
+  const uint32_t s1 = lop3<0x96>(a, b, c);  // a ^ b ^ c
+  const uint32_t c1 = lop3<0xE8>(a, b, c);  // majority
+  Classes r;
+  r.ge2 = lop3<0xF8>(c1, s1, d);  // c1 | (s1 & d): >= 2 positive   (Delta >= 0, unmasked)
+  r.k4 = lop3<0x80>(c1, s1, d);   // c1 & s1 & d:     4 positive     (Delta = +4)
+  r.k3 = lop3<0x60>(c1, s1, d);   // c1 & (s1 ^ d):   3 positive     (Delta = +2)
+  r.km4 = lop3<0x01>(c1, s1, d);  // ~(c1 | s1 | d):  0 positive     (Delta = -4)
+  r.km2 = lop3<0x06>(c1, s1, d);  // ~c1 & (s1 ^ d):  1 positive     (Delta = -2)
+  return r;
+}
+
 // Bit-sliced comparison of the uniforms' top 8 bits with the thresholds, as a
 // borrow chain over the planes LSB-first (plane 7 = uniform bit 24 first,
 // plane 0 = bit 31 last).  c2 = class -2 sites (threshold K2), other pending
@@ -62,9 +104,9 @@ __device__ __forceinline__ Classes classes(uint32_t Sw, uint32_t same, uint32_t 
 // sites whose 8 bits all equal K_hi.  3 LOP3 per plane.
 __device__ __forceinline__ void cmp_plane_lsb(uint32_t R, uint32_t c2, uint32_t ma, uint32_t mb,
                                               uint32_t &eq, uint32_t &lt) {
-  const uint32_t tb = (c2 & ma) | (~c2 & mb);
-  lt = (tb & (~R | lt)) | (~tb & ~R & lt);
-  eq &= ~(R ^ tb);
+  const uint32_t tb = lop3<0xCA>(c2, ma, mb);  // c2 ? ma : mb
+  lt = lop3<0xB2>(tb, R, lt);                  // tb ? (~R | lt) : (~R & lt)
+  eq = lop3<0x90>(eq, R, tb);                  // eq & ~(R ^ tb)
 }
 
 // 8-bit mask of the non-zero nibbles of x (bit g <-> nibble g)
