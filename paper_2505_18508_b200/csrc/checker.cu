@@ -429,14 +429,26 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
               basep += rtot[j];
             }
             excl[j] += wbase;
-            if (own[j] && wpos[j] > 0 && cur + excl[j] + wpos[j] > best) cand = true;
           }
+          // Every word end is an achieved value, so the maximum M is at least
+          // the largest of them (Lmax; warp-local for larger teams), and a word
+          // can hold a position of value >= Lmax only if its bound cur + excl +
+          // wpos reaches Lmax.  Candidates: bound >= max(best + 1, Lmax).
+          int lmax = INT_MIN;
+#pragma unroll
+          for (int j = 0; j < WPT; j++)
+            if (own[j]) lmax = max(lmax, excl[j] + wsum[j]);
+          lmax = __reduce_max_sync(0xffffffffu, lmax);
+          const int thr = max(best + 1, cur + lmax);
+#pragma unroll
+          for (int j = 0; j < WPT; j++)
+            if (own[j] && wpos[j] > 0 && cur + excl[j] + wpos[j] >= thr) cand = true;
           const bool anyc = NWARP > 1 ? __syncthreads_or(cand) : __any_sync(0xffffffffu, cand);
           if (anyc) {
             long long key = LLONG_MIN;
 #pragma unroll
             for (int j = 0; j < WPT; j++) {
-              if (!own[j] || wpos[j] <= 0 || cur + excl[j] + wpos[j] <= best) continue;
+              if (!own[j] || wpos[j] <= 0 || cur + excl[j] + wpos[j] < thr) continue;
               // recompute the classes of the pre-phase word (neighbours unchanged)
               const int wi = j * NT + tid;
               const uint4 g = geo[wi];
@@ -664,13 +676,13 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.err = err_ws;
   a.blocks = (unsigned long long *)((char *)err_ws + 8);
   const bool sa = kind == GSB_ANNEALING;
-  // Team shape: W warps per trial (power of two), WPT words per lane.  As few
-  // warps per trial as possible: a one-warp team needs no CTA barriers at all
-  // (measured best up to WPT = 8); larger teams keep WPT <= 6.  Grow the team
-  // only while the trials cannot give every SM at least two warps.
+  // Team shape: W warps per trial (power of two), WPT <= 8 words per lane.
+  // As few warps per trial as possible (a one-warp team needs no CTA barriers
+  // at all; fewer, longer lanes have more ILP); grow the team only while the
+  // words do not fit or the trials cannot give every SM at least two warps.
   int W = 1;
   while (W < 16 && 32 * W < nw &&
-         ((long long)T * W < 2LL * nsm || (nw + 32 * W - 1) / (32 * W) > (W == 1 ? 8 : 6)))
+         ((long long)T * W < 2LL * nsm || (nw + 32 * W - 1) / (32 * W) > 8))
     W *= 2;
   if (const char *ov = getenv("GSB_CHECKER_WARPS")) {  // development tuning knob
     const int w = atoi(ov);
