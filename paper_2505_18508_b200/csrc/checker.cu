@@ -203,14 +203,18 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
     int buf = 0;
 
     for (int t = 0; t < a.sweeps; t++) {
-      uint32_t K2 = 0, K4 = 0;
-      bool all2 = false, all4 = false;
+      // K >= 2^32 (always accept) is emulated exactly by K_hi = 0xFF and a
+      // tail threshold of 2^24 (every tie accepts); K = 0 (never) drops the
+      // class from the pending sites (me = 0), so it draws nothing.
+      uint32_t K2 = 0, K4 = 0, K2lo = 0, K4lo = 0, me2 = 0, me4 = 0;
       if (SA) {
         const uint64_t t2 = a.table[(size_t)t * 4 + 1], t4 = a.table[(size_t)t * 4 + 3];
-        all2 = t2 > 0xFFFFFFFFull;
-        all4 = t4 > 0xFFFFFFFFull;
-        K2 = (uint32_t)t2;
-        K4 = (uint32_t)t4;
+        K2 = t2 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t2;
+        K4 = t4 > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t4;
+        K2lo = t2 > 0xFFFFFFFFull ? 0x1000000u : (K2 & 0xFFFFFFu);
+        K4lo = t4 > 0xFFFFFFFFull ? 0x1000000u : (K4 & 0xFFFFFFu);
+        me2 = t2 ? ~0u : 0u;
+        me4 = t4 ? ~0u : 0u;
       }
       // per-sweep plane masks (bits 31..24 of K2 / K4)
       uint32_t ma[8], mb[8];
@@ -219,7 +223,6 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
         ma[q] = (uint32_t)((int32_t)(K2 << q) >> 31);
         mb[q] = (uint32_t)((int32_t)(K4 << q) >> 31);
       }
-      const uint32_t K2lo = K2 & 0xFFFFFFu, K4lo = K4 & 0xFFFFFFu;
       bool sweep_flipped = false;
 #pragma unroll 1
       for (int p = 0; p < 2; p++, buf ^= 1) {
@@ -243,20 +246,9 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
             const Classes c = classes_pad(cur_w[j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m);
             wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
             if (SA) {
-              uint32_t b = c.ge2 & g.w;
-              int neg = 0;
-              if (all2) {
-                b |= c.km2;
-                neg += 2 * __popc(c.km2);
-              }
-              if (all4) {
-                b |= c.km4;
-                neg += 4 * __popc(c.km4);
-              }
-              A[j] = b;
-              wsum[j] = wpos[j] - neg;
-              const uint32_t e2 = (all2 || K2 == 0) ? 0u : c.km2;
-              const uint32_t e4 = (all4 || K4 == 0) ? 0u : c.km4;
+              A[j] = c.ge2 & g.w;
+              wsum[j] = wpos[j];  // minus the accepted Delta<0 flips at commit
+              const uint32_t e2 = c.km2 & me2, e4 = c.km4 & me4;
               c2[j] = e2;
               const uint32_t pend = e2 | e4;
               uint32_t q = pend, l = 0;
