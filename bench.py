@@ -117,8 +117,9 @@ class ClockSampler:
 def cpu_port_rate(rows, cols, sweeps, seconds_target, threads=None):
     """Reference algorithm (oracle C port of solvers.run_trial) on host cores.
 
-    Bounded sample: `threads` trials x the FULL sweep schedule when that fits
-    the time target, otherwise a prefix of the sweeps is timed (rate only).
+    Bounded sample: `threads` trials (or a multiple of it) x the FULL sweep
+    schedule when that fits the time target, otherwise a prefix of the sweeps
+    is timed (rate only).
     """
     from oracle import oracle as O
 
@@ -133,13 +134,16 @@ def cpu_port_rate(rows, cols, sweeps, seconds_target, threads=None):
                      spins=False, nthreads=1)
     per_upd = (time.perf_counter() - t0) / (20 * n)
     s_budget = max(10, min(sweeps, int(seconds_target / max(per_upd * n, 1e-12))))
-    seeds = [O.mix_seed(MASTER, i) for i in range(threads)]
+    rounds = 1
+    if s_budget == sweeps:  # whole schedules fit: as many trial rounds as the target allows
+        rounds = max(1, min(16, int(seconds_target / max(per_upd * n * sweeps, 1e-12))))
+    seeds = [O.mix_seed(MASTER, i) for i in range(threads * rounds)]
     t0 = time.perf_counter()
     _, _, se = O.run_trials_ref(n, eu, ev, ew, "simulated_annealing", s_budget, seeds, 3.0, 0.05,
                                 spins=False, nthreads=threads)
     dt = time.perf_counter() - t0
     upd = int(se.sum()) * n
-    sample = (f"{threads} trials x {s_budget} sweeps of reference SA (PCG64 + permutation, "
+    sample = (f"{threads * rounds} trials x {s_budget} sweeps of reference SA (PCG64 + permutation, "
               f"schedule 3.0->0.05 over {s_budget} sweeps) on torus {rows}x{cols}:1, "
               f"{threads} host threads")
     return upd / dt, threads, sample, dt
