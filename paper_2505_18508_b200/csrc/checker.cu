@@ -99,10 +99,35 @@ __global__ void checker_masks_kernel(int rows, int cols, int WPR, const int8_t *
   }
 }
 
+// Per-colour neighbour table for the sweep kernel, geo2[p][wi] = two uint4:
+//   {up, down, carry word: byte offsets into the spin copy of colour p^1
+//    (relative to st), V},
+//   {VG, r, a, b}: the shifted neighbour is rot(same, r) & VG | (x << a) >> b,
+//    x = the carry word; r = 1 (k-1 neighbour) or 31 (k+1, a right rotate),
+//    VG = V minus the bit the rotate wraps around, a = 31 - src bit,
+//    b = 31 - dst bit (the carry lands on exactly one valid bit).
+// Read through the L1 (shared by every CTA on the SM), not staged per CTA.
+__global__ void checker_geo2_kernel(int nw, const uint4 *__restrict__ geo, uint4 *__restrict__ geo2) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * nw;
+       idx += gridDim.x * blockDim.x) {
+    const int p = idx / nw, wi = idx % nw;
+    const uint4 g = geo[wi];
+    const uint32_t base = (uint32_t)((p ^ 1) * nw);
+    const uint32_t cidx = p ? (g.y >> 16) : (g.y & 0xFFFFu);
+    const uint32_t cinfo = p ? (g.z >> 16) : (g.z & 0xFFFFu);
+    const uint32_t src = cinfo & 31u, dst = (cinfo >> 5) & 31u, dir = (cinfo >> 10) & 1u;
+    geo2[2 * idx] = make_uint4((base + (g.x & 0xFFFFu)) * 4u, (base + (g.x >> 16)) * 4u,
+                               (base + cidx) * 4u, g.w);
+    geo2[2 * idx + 1] = make_uint4(g.w & ~(dir ? 0x80000000u : 1u), dir ? 31u : 1u, 31u - src,
+                                   31u - dst);
+  }
+}
+
 struct CheckerArgs {
   int rows, cols, H, WPR, nw, lb;
   const uint4 *masks;
   const uint4 *geo;
+  const uint4 *geo2;
   const uint64_t *table;  // [S][4]
   int sweeps;
   const uint64_t *seeds;
@@ -125,9 +150,11 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
   static_assert(WPT <= 8, "tail items pack (lane, word) as lane << 3 | j");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nw = a.nw;
-  uint4 *msk = (uint4 *)smem_raw;                 // [2][nw]
-  uint4 *geo = msk + 2 * nw;                      // [nw]
-  uint32_t *st = (uint32_t *)(geo + nw);          // [2][nw] neighbour copy
+  // instance tables (identical for every trial) are read through the L1
+  const uint4 *__restrict__ msk = a.masks;        // [2][nw]
+  const uint4 *__restrict__ geo = a.geo;          // [nw]
+  const uint4 *__restrict__ geo2 = a.geo2;        // [2][nw][2]
+  uint32_t *st = (uint32_t *)smem_raw;            // [2][nw] neighbour copy
   uint32_t *bst = st + 2 * nw;                    // [2][nw] best snapshot
   uint32_t *tx = bst + 2 * nw;                    // [NWARP][3][WPT][32] tail exchange
   uint32_t *tq = tx + NWARP * 3 * WPT * 32;       // [NWARP][32] tail queue
@@ -145,8 +172,6 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
   uint32_t *myq = tq + warp * 32;
   unsigned *wctr = wctrs + warp;
 
-  for (int i = tid; i < 2 * nw; i += NT) msk[i] = a.masks[i];
-  for (int i = tid; i < nw; i += NT) geo[i] = a.geo[i];
   for (int i = tid; i < NWARP * 3 * WPT * 32; i += NT) tx[i] = 0;
   if (tid < NWARP) wctrs[tid] = 0;
   __syncthreads();
@@ -226,7 +251,6 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
       bool sweep_flipped = false;
 #pragma unroll 1
       for (int p = 0; p < 2; p++, buf ^= 1) {
-        const uint32_t *o = st + (p ^ 1) * nw;
         uint32_t A[WPT], c2[WPT], eq[WPT], lt[WPT];
         int wpos[WPT], wsum[WPT];
         // ---- pass 1: classes and the unconditional planes 0-7.  Words j <
@@ -238,15 +262,15 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
           A[j] = c2[j] = eq[j] = lt[j] = 0;
           wpos[j] = wsum[j] = 0;
           if (j < WPT - 1 || own[j]) {
-            const uint4 g = geo[wi];
-            const uint4 m = msk[p * nw + wi];
+            const uint4 ga = __ldg(&geo2[2 * (p * nw + wi)]);
+            const uint4 gb = __ldg(&geo2[2 * (p * nw + wi) + 1]);
+            const uint4 m = __ldg(&msk[p * nw + wi]);
             const uint32_t same = oth_w[j];
-            const uint32_t sh = shifted_nb_v(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
-                                             p ? (g.z >> 16) : (g.z & 0xFFFFu), g.w);
-            const Classes c = classes_pad(cur_w[j], same, sh, o[g.x & 0xFFFFu], o[g.x >> 16], m);
+            const uint32_t sh = shifted_nb2(st, same, ga, gb);
+            const Classes c = classes_pad(cur_w[j], same, sh, word_at(st, ga.x), word_at(st, ga.y), m);
             wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
             if (SA) {
-              A[j] = c.ge2 & g.w;
+              A[j] = c.ge2 & ga.w;
               wsum[j] = wpos[j];  // minus the accepted Delta<0 flips at commit
               const uint32_t e2 = c.km2 & me2, e4 = c.km4 & me4;
               c2[j] = e2;
@@ -443,13 +467,13 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
               if (!own[j] || wpos[j] <= 0 || cur + excl[j] + wpos[j] < thr) continue;
               // recompute the classes of the pre-phase word (neighbours unchanged)
               const int wi = j * NT + tid;
-              const uint4 g = geo[wi];
+              const uint4 ga = __ldg(&geo2[2 * (p * nw + wi)]);
+              const uint4 gb = __ldg(&geo2[2 * (p * nw + wi) + 1]);
               const uint32_t Sold = cur_w[j] ^ A[j];
               const uint32_t same = oth_w[j];
-              const uint32_t sh = shifted_nb_v(o, same, p ? (g.y >> 16) : (g.y & 0xFFFFu),
-                                               p ? (g.z >> 16) : (g.z & 0xFFFFu), g.w);
-              const Classes c = classes_pad(Sold, same, sh, o[g.x & 0xFFFFu], o[g.x >> 16],
-                                            msk[p * nw + wi]);
+              const uint32_t sh = shifted_nb2(st, same, ga, gb);
+              const Classes c = classes_pad(Sold, same, sh, word_at(st, ga.x), word_at(st, ga.y),
+                                            __ldg(&msk[p * nw + wi]));
               const uint32_t Aj = A[j];
               const uint32_t P2 = Aj & c.k3, P4m = Aj & c.k4, N2 = Aj & c.km2, N4 = Aj & c.km4;
               int v = cur + excl[j], mx = INT_MIN, mp = -1;
@@ -572,8 +596,7 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
 // ------------------------------------------------------------------ launch
 static size_t smem_bytes(int nw, int NT, int WPT) {
   const int NWARP = NT / 32;
-  size_t b = (size_t)3 * nw * 16;                           // msk, geo
-  b += (size_t)4 * nw * 4;                                  // st, bst
+  size_t b = (size_t)4 * nw * 4;                            // st, bst
   b += (size_t)NWARP * 3 * WPT * 32 * 4 + (size_t)NWARP * 32 * 4;  // tail exchange + queue
   b += (size_t)(6 * NWARP) * 4;
   b += (size_t)((WPT * NWARP + 1) & ~1) * 4;
@@ -620,7 +643,8 @@ bool checker_fits(int rows, int cols) {
 size_t checker_workspace_bytes(int rows, int cols) {
   int WPR, nw;
   checker_words(rows, cols, &WPR, &nw);
-  return align_up((size_t)2 * nw * 16, 256) + align_up((size_t)nw * 16, 256);
+  return align_up((size_t)2 * nw * 16, 256) + align_up((size_t)nw * 16, 256) +
+         align_up((size_t)2 * nw * 32, 256);
 }
 
 template <int WPT>
@@ -646,6 +670,7 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   if (nsm <= 0) return set_error(GSB_ECUDA, "no CUDA device");
   uint4 *masks = (uint4 *)ws;
   uint4 *geo = (uint4 *)((char *)ws + align_up((size_t)2 * nw * 16, 256));
+  uint4 *geo2 = (uint4 *)((char *)geo + align_up((size_t)nw * 16, 256));
   checker_masks_kernel<<<(2 * nw + 255) / 256, 256, 0, stream>>>(rows, cols, WPR, w_dev, masks,
                                                                  geo);
   CheckerArgs a;
@@ -655,8 +680,10 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.WPR = WPR;
   a.nw = nw;
   a.lb = (a.H - 1) & 31;
+  checker_geo2_kernel<<<(2 * nw + 255) / 256, 256, 0, stream>>>(nw, geo, geo2);
   a.masks = masks;
   a.geo = geo;
+  a.geo2 = geo2;
   a.table = table;
   a.sweeps = sweeps;
   a.seeds = seeds;

@@ -73,6 +73,20 @@ __device__ __forceinline__ uint32_t shifted_nb_v(const uint32_t *__restrict__ o,
   return lop3<0xA8>(t, carry, V);  // (t | carry) & V
 }
 
+// word at a byte offset into the shared spin copy
+__device__ __forceinline__ uint32_t word_at(const uint32_t *base, uint32_t off) {
+  return *(const uint32_t *)((const char *)base + off);
+}
+
+// Shifted neighbour from the per-colour table of checker_geo2_kernel:
+// ga = {up, down, carry offsets, V}, gb = {VG, r, a, b}.  4 ALU ops.
+__device__ __forceinline__ uint32_t shifted_nb2(const uint32_t *st, uint32_t same, uint4 ga,
+                                                uint4 gb) {
+  const uint32_t rot = __funnelshift_l(same, same, gb.y);  // rotate left by r
+  const uint32_t carry = (word_at(st, ga.z) << gb.z) >> gb.w;
+  return lop3<0xEA>(rot, gb.x, carry);  // (rot & VG) | carry
+}
+
 // Delta classes in 11 LOP3s, using the padding convention of
 // checker_masks_kernel (coupling planes NU/ND set, NS/NSH clear on padding
 // bits) and padding-free spin/neighbour words: a padding site then has
