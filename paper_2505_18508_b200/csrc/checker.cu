@@ -13,8 +13,10 @@
 //   H = cols/2 sites per row per colour, WPR = ceil(H/32), padding bits 0.
 // One CTA runs one trial at a time (persistent over trials).  Thread `tid`
 // owns words wi = j*NT + tid (j < WPT) of BOTH colours and keeps them in
-// registers; shared memory holds the copy its neighbours read, the couplings
-// (4 sign planes per word, uint4) and the best-so-far snapshot.
+// registers; shared memory holds the copy its neighbours read and the
+// best-so-far snapshot.  The instance tables (coupling sign planes, neighbour
+// offsets) are the same for every trial and are read through the L1, which
+// all CTAs on an SM share.
 //
 // Per word and half-sweep: 4 positive-term planes P_j = ~(S^N_j^NEG_j),
 // bit-sliced counts -> Delta classes, then for the Delta<0 sites a bit-sliced
