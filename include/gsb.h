@@ -51,7 +51,10 @@ extern "C" {
 #define GSB_ENGINE_REFERENCE 0    /* numpy-PCG64 + random permutation: bit-exact with run_trial */
 #define GSB_ENGINE_CHECKERBOARD 1 /* Philox4x32-10 + colour order (DESIGN.md contract)        */
 #define GSB_ENGINE_CHECKERBOARD_TILED 2 /* same contract, forces the HBM-tiled engine (used
-                                           automatically when the torus exceeds shared memory) */
+                                           automatically when the torus exceeds a cluster) */
+#define GSB_ENGINE_CHECKERBOARD_CLUSTER 3 /* same contract, forces the cluster engine (one trial
+                                             over the shared memory of a CTA cluster; used
+                                             automatically when the torus exceeds one SM) */
 
 typedef struct gsb_torus {
     int32_t rows, cols;  /* TorusSpec.rows/cols (instances.py:186-187), >= 3 */

@@ -416,6 +416,12 @@ static int trial_checker(int32_t rows, int32_t cols, const int8_t *w, const int3
     int64_t current = gso_cut(m, eu, ev, ew, s);
     int64_t best = current;
     memcpy(bs, s, (size_t)n);
+    /* best_spins = tuple(spins) at every new best (solvers.py:125-127),
+       materialised once per half-sweep: the flips of the half-sweep are logged
+       and, if the best improved in it, bs = s minus the flips after the last
+       improvement (same snapshot, O(n) per half-sweep instead of per event). */
+    int32_t *flog = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int64_t nlog = 0, nbest = -1;
     int32_t executed = 0;
     int annealing = kind == GSO_ANNEALING;
     plane_cache pc;
@@ -425,7 +431,9 @@ static int trial_checker(int32_t rows, int32_t cols, const int8_t *w, const int3
     for (int32_t sweep = 0; sweep < sweeps; sweep++) {
         double temp = annealing ? gso_temperature(sweeps, t0, t1, sweep) : 0.0;
         int flipped = 0;
-        for (int32_t p = 0; p < 2; p++)
+        for (int32_t p = 0; p < 2; p++) {
+            nlog = 0;
+            nbest = -1;
             for (int32_t r = 0; r < rows; r++)
                 for (int32_t k = 0; k < H; k++) {
                     int32_t c = 2 * k + ((r + p) & 1);
@@ -451,15 +459,22 @@ static int trial_checker(int32_t rows, int32_t cols, const int8_t *w, const int3
                         s[i] = (int8_t)-s[i];
                         current += delta;
                         flipped = 1;
+                        flog[nlog++] = i;
                         if (current > best) {
                             best = current;
-                            memcpy(bs, s, (size_t)n);
+                            nbest = nlog;
                         }
                     }
                 }
+            if (nbest >= 0) {
+                memcpy(bs, s, (size_t)n);
+                for (int64_t f = nbest; f < nlog; f++) bs[flog[f]] = (int8_t)-bs[flog[f]];
+            }
+        }
         executed = sweep + 1;
         if (!annealing && !flipped) break;
     }
+    free(flog);
     int rc = 0;
     if (best != gso_cut(m, eu, ev, ew, bs)) rc = -1;
     *best_cut = best;

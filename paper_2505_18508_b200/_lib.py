@@ -26,6 +26,7 @@ GSB_ANNEALING = 1
 ENGINE_REFERENCE = 0
 ENGINE_CHECKERBOARD = 1
 ENGINE_CHECKERBOARD_TILED = 2
+ENGINE_CHECKERBOARD_CLUSTER = 3
 
 _lock = threading.Lock()
 _lib = None

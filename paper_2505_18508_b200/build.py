@@ -15,7 +15,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libgsb_cuda.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "refexact.cu", "refexact_warp.cu",
+SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "checker_cluster.cu", "refexact.cu", "refexact_warp.cu",
            "evaluate.cu"]
 HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh"]
 

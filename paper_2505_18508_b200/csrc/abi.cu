@@ -131,7 +131,8 @@ int gsb_schedule_table(int engine, int32_t sweeps, double t0, double t1, int32_t
   int bits;
   if (engine == GSB_ENGINE_REFERENCE)
     bits = 53;
-  else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED)
+  else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
+           engine == GSB_ENGINE_CHECKERBOARD_CLUSTER)
     bits = 32;
   else
     return set_error(GSB_EINVAL, "unknown engine");
@@ -154,7 +155,11 @@ size_t gsb_torus_workspace_bytes(const gsb_torus *inst, int engine, int32_t swee
   size_t b = err_bytes();
   if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
     b += checker_workspace_bytes(inst->rows, inst->cols);
-  } else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED) {
+  } else if ((engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_CLUSTER) &&
+             checker_cluster_fits(inst->rows, inst->cols)) {
+    b += checker_cluster_workspace_bytes(inst->rows, inst->cols);
+  } else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
+             engine == GSB_ENGINE_CHECKERBOARD_CLUSTER) {
     b += checker_hbm_workspace_bytes(inst->rows, inst->cols, T, num_sms());
   } else {
     b += ref_workspace_bytes(n, 0, T);
@@ -194,14 +199,20 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   if (cudaMemsetAsync(err, 0, 16, stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
   int rc;
-  if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED) {
+  if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
+      engine == GSB_ENGINE_CHECKERBOARD_CLUSTER) {
     if ((inst->rows & 1) || (inst->cols & 1))
       return set_error(GSB_EUNSUPPORTED,
                        "checkerboard kinds need even torus dimensions (bipartite torus)");
     if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
       rc = checker_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
                        best_cut, sweeps_exec, best_bits, rest, err, stream);
-    } else if (checker_hbm_fits(inst->rows, inst->cols)) {
+    } else if (engine != GSB_ENGINE_CHECKERBOARD_TILED &&
+               checker_cluster_fits(inst->rows, inst->cols)) {
+      rc = checker_cluster_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
+                               best_cut, sweeps_exec, best_bits, rest, err, stream);
+    } else if (engine != GSB_ENGINE_CHECKERBOARD_CLUSTER &&
+               checker_hbm_fits(inst->rows, inst->cols)) {
       rc = checker_hbm_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
                            best_cut, sweeps_exec, best_bits, rest, err, stream);
     } else {

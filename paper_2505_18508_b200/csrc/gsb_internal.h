@@ -31,6 +31,14 @@ int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweep
                     int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                     cudaStream_t stream);
 
+// cluster checkerboard engine (checker_cluster.cu)
+bool checker_cluster_fits(int rows, int cols);
+size_t checker_cluster_workspace_bytes(int rows, int cols);
+int checker_cluster_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+                        const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
+                        int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
+                        cudaStream_t stream);
+
 // reference-exact engines (refexact.cu: any graph; refexact_warp.cu: tori, n < 2^16)
 bool ref_warp_fits(int rows, int cols);
 int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
