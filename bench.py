@@ -2,7 +2,7 @@
 """Benchmark of the sweep hot path (BASELINE.json metric: spin-updates/s).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c1|c2|c3|c4] [--kind KIND]
+                    [--config c1|c2|c3|c4|c5] [--kind KIND]
 
 One *step* = one batched campaign over this rank's trials: T trials x S sweeps
 of simulated annealing (default schedule 3.0 -> 0.05, solvers.py:31-32) on the
@@ -40,6 +40,9 @@ CONFIGS = {
     "c2": (100, 100, 1024, 10_000),
     "c3": (100, 140, 4096, 20_000),
     "c4": (100, 200, 8192, 50_000),
+    # configs[4]: 64 trials (sharded over 8 GPUs in BASELINE; weak scaling here,
+    # 64 per GPU); beyond one SM -> the cluster engine (16-CTA cluster / trial)
+    "c5": (2000, 2000, 64, 1000),
 }
 MASTER = 20250814
 L2_BYTES = 126 * 1024 * 1024
@@ -370,7 +373,9 @@ def main():
     torch.cuda.synchronize()
     philox_peak = nthr * bpt / (pe0.elapsed_time(pe1) / 1e3)  # blocks/s
 
-    # ---- roofline of the dominant kernel (the sweep kernel)
+    # ---- roofline of the dominant kernel (the sweep kernel of this torus)
+    sweep_kernel = ("gsb::checker_sweep_kernel" if (cols // 2 + 31) // 32 * rows <= 2048
+                    else "gsb::checker_cluster_kernel")
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -387,7 +392,7 @@ def main():
         "bound": "int", "unit": "Gblock/s (Philox4x32-10)",
         "achieved": rng_achieved / 1e9, "peak": philox_peak / 1e9,
         "frac": rng_achieved / philox_peak, "traffic": None,
-        "kernel": "gsb::checker_sweep_kernel",
+        "kernel": sweep_kernel,
         "algorithmic_units_per_launch": blocks_per_step,
         "unit_def": "Philox4x32-10 blocks the checkerboard contract requires (2 init + 8 "
                     "planes per word and half-sweep + per-site tail groups), counted by the kernel",
@@ -407,7 +412,7 @@ def main():
     # ---- secondary: the bit-exact reference engine (kinds of the reference)
     # on the same torus, 1024 trials x 1000 sweeps (its own 3.0->0.05 schedule)
     ref_engine = None
-    if not a.no_ref_engine:
+    if not a.no_ref_engine and n < 65536:  # its warp engine needs n < 2^16
         from paper_2505_18508_b200.solvers import run_trials_device
 
         rcfg = default_config("simulated_annealing", 1000, 0)

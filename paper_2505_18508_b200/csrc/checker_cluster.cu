@@ -104,6 +104,14 @@ __host__ __device__ inline ClLayout cl_layout(int Rmax, int WPR, int WPT) {
   return L;
 }
 
+// max of a 64-bit key (value << 32 | tie-break) over the warp: two REDUX ops
+__device__ __forceinline__ long long warp_max_key(long long key) {
+  const int hi = (int)(key >> 32);
+  const int mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? (unsigned)key : 0u);
+  return (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
+}
+
 __device__ __forceinline__ void cl_arrive_wait() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -249,8 +257,7 @@ __global__ void __launch_bounds__(CL_NT, 1) checker_cluster_kernel(ClusterArgs a
     //  cw/aq: the other colour now and its flips since)
     auto resolve = [&](int pp, const uint32_t *ow, const uint32_t *cw, const uint32_t *aq,
                        int slot) {
-      long long key = LLONG_MIN;
-      for (int i = 0; i < C; i++) key = sh.keys[slot][i] > key ? sh.keys[slot][i] : key;
+      const long long key = warp_max_key(lane < C ? sh.keys[slot][lane] : LLONG_MIN);
       const int mval = (int)(key >> 32);
       if (key == LLONG_MIN || mval <= best) return;
       best = mval;
@@ -453,12 +460,13 @@ __global__ void __launch_bounds__(CL_NT, 1) checker_cluster_kernel(ClusterArgs a
 
         // ---- after the barrier: resolve half-sweep h-1, then this one's sums
         if (pend_prev) resolve(p ^ 1, oth_w, cur_w, A, slot ^ 1);
-        int D = 0, Pt = 0, pre = 0;
-        for (int i = 0; i < C; i++) {
-          const int d = sh.part[slot][0][i];
-          D += d;
-          Pt += sh.part[slot][1][i];
-          if (i < q) pre += d;
+        int D, Pt, pre;
+        {
+          const int d = lane < C ? sh.part[slot][0][lane] : 0;
+          const int pp = lane < C ? sh.part[slot][1][lane] : 0;
+          D = (int)__reduce_add_sync(0xffffffffu, (unsigned)d);
+          Pt = (int)__reduce_add_sync(0xffffffffu, (unsigned)pp);
+          pre = (int)__reduce_add_sync(0xffffffffu, (unsigned)(lane < q ? d : 0));
         }
         if (Pt > 0) sweep_flipped = true;  // greedy flips are exactly the positive ones
         const bool pend = cur + Pt > best;  // uniform over the cluster
@@ -564,16 +572,10 @@ __global__ void __launch_bounds__(CL_NT, 1) checker_cluster_kernel(ClusterArgs a
                                    (long long)(0xFFFFFFFFu - (uint32_t)pos);
               key = kk > key ? kk : key;
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              const long long y = __shfl_xor_sync(0xffffffffu, key, off);
-              key = y > key ? y : key;
-            }
+            key = warp_max_key(key);
             if (lane == 0) sh.kred[warp] = key;
             __syncthreads();
-            key = LLONG_MIN;
-#pragma unroll
-            for (int i = 0; i < NWARP; i++) key = sh.kred[i] > key ? sh.kred[i] : key;
+            key = warp_max_key(lane < NWARP ? sh.kred[lane] : LLONG_MIN);
           }
           if (tid < C) *cl.map_shared_rank(&sh.keys[slot][q], tid) = key;
         }
