@@ -133,9 +133,10 @@ def cpu_port_rate(rows, cols, sweeps, seconds_target, threads=None):
     eu, ev, ew = O.torus_edges(rows, cols, w)
     # calibrate on one short trial
     t0 = time.perf_counter()
-    O.run_trials_ref(n, eu, ev, ew, "simulated_annealing", 20, [O.mix_seed(MASTER, 0)], 3.0, 0.05,
+    cal = max(1, min(20, 200_000 // n))  # calibration sweeps: ~0.2 s
+    O.run_trials_ref(n, eu, ev, ew, "simulated_annealing", cal, [O.mix_seed(MASTER, 0)], 3.0, 0.05,
                      spins=False, nthreads=1)
-    per_upd = (time.perf_counter() - t0) / (20 * n)
+    per_upd = (time.perf_counter() - t0) / (cal * n)
     s_budget = max(10, min(sweeps, int(seconds_target / max(per_upd * n, 1e-12))))
     rounds = 1
     if s_budget == sweeps:  # whole schedules fit: as many trial rounds as the target allows

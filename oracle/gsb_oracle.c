@@ -306,11 +306,15 @@ static int trial_ref_csr(const csr_t *G, int64_t m, const int32_t *eu, const int
     int64_t current = gso_cut(m, eu, ev, ew, s); /* :101 */
     int64_t best = current;
     memcpy(bs, s, (size_t)n);
+    /* best_spins = tuple(spins) at every new best (:125-127), materialised once
+       per sweep from the sweep's flip log (same snapshot, O(n) per sweep) */
+    int32_t *flog = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     int32_t executed = 0;
     int annealing = kind == GSO_ANNEALING;
     for (int32_t sweep = 0; sweep < sweeps; sweep++) { /* :107 */
         double temp = annealing ? gso_temperature(sweeps, t0, t1, sweep) : 0.0;
         int flipped = 0;
+        int64_t nlog = 0, nbest = -1;
         gso_pcg64_permutation(&g, n, perm); /* :110 */
         for (int32_t k = 0; k < n; k++) {
             int32_t i = (int32_t)perm[k];
@@ -327,15 +331,21 @@ static int trial_ref_csr(const csr_t *G, int64_t m, const int32_t *eu, const int
                 s[i] = (int8_t)-s[i];
                 current += delta;
                 flipped = 1;
+                flog[nlog++] = i;
                 if (current > best) { /* :125-127 */
                     best = current;
-                    memcpy(bs, s, (size_t)n);
+                    nbest = nlog;
                 }
             }
+        }
+        if (nbest >= 0) {
+            memcpy(bs, s, (size_t)n);
+            for (int64_t f = nbest; f < nlog; f++) bs[flog[f]] = (int8_t)-bs[flog[f]];
         }
         executed = sweep + 1;
         if (!annealing && !flipped) break; /* :129-130 */
     }
+    free(flog);
     int rc = 0;
     if (best != gso_cut(m, eu, ev, ew, bs)) rc = -1; /* :132-133 */
     *best_cut = best;
