@@ -140,6 +140,7 @@ struct CheckerArgs {
   int nbytes;
   int *err;
   unsigned long long *blocks;  // Philox blocks drawn (statistics, workspace)
+  int zp_max;                  // largest comparator specialisation used (8; dev knob)
 };
 
 
@@ -243,13 +244,13 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
         me2 = t2 ? ~0u : 0u;
         me4 = t4 ? ~0u : 0u;
       }
-      // per-sweep plane masks (bits 31..24 of K2 / K4)
-      uint32_t ma[8], mb[8];
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        ma[q] = (uint32_t)((int32_t)(K2 << q) >> 31);
-        mb[q] = (uint32_t)((int32_t)(K4 << q) >> 31);
-      }
+      // comparator specialisation (uniform per sweep), where registers allow
+      // the extra code paths (measured, tools/zp_ab.py): 256 registers
+      // (config 2) L <= 8, +3.5 %; 128 registers and <= 5 words per lane
+      // (configs 1, 3) L <= 4, +2 %; 7 words at 128 registers (config 4):
+      // none (the specialised bodies spill, -10 %).
+      constexpr int kZp = !SA ? 0 : 65536 / (NT * MINB) >= 200 ? 8 : WPT <= 5 ? 4 : 0;
+      const int zp = kZp ? min(min(zero_planes(K2, K4), a.zp_max), kZp) : 0;
       bool sweep_flipped = false;
 #pragma unroll 1
       for (int p = 0; p < 2; p++, buf ^= 1) {
@@ -258,46 +259,43 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
         // ---- pass 1: classes and the unconditional planes 0-7.  Words j <
         // WPT-1 are owned by every lane (the launch picks WPT = ceil(nw/NT)),
         // so only the last one is guarded and the bodies schedule together.
+        auto pass1 = [&](auto Lc) {
+          constexpr int L = decltype(Lc)::value;
 #pragma unroll
-        for (int j = 0; j < WPT; j++) {
-          const int wi = j * NT + tid;
-          A[j] = c2[j] = eq[j] = lt[j] = 0;
-          wpos[j] = wsum[j] = 0;
-          if (j < WPT - 1 || own[j]) {
-            const uint4 ga = __ldg(&geo2[2 * (p * nw + wi)]);
-            const uint4 gb = __ldg(&geo2[2 * (p * nw + wi) + 1]);
-            const uint4 m = __ldg(&msk[p * nw + wi]);
-            const uint32_t same = oth_w[j];
-            const uint32_t sh = shifted_nb2(st, same, ga, gb);
-            const Classes c = classes_pad(cur_w[j], same, sh, word_at(st, ga.x), word_at(st, ga.y), m);
-            wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
-            if (SA) {
-              A[j] = c.ge2 & ga.w;
-              wsum[j] = wpos[j];  // minus the accepted Delta<0 flips at commit
-              const uint32_t e2 = c.km2 & me2, e4 = c.km4 & me4;
-              c2[j] = e2;
-              const uint32_t pend = e2 | e4;
-              uint32_t q = pend, l = 0;
-              const P4 r0 =
-                  philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p), 1u}, key0, key1);
-              const P4 r1 =
-                  philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p + 1), 1u}, key0, key1);
-              cmp_plane_lsb(r1.w, e2, ma[7], mb[7], q, l);
-              cmp_plane_lsb(r1.z, e2, ma[6], mb[6], q, l);
-              cmp_plane_lsb(r1.y, e2, ma[5], mb[5], q, l);
-              cmp_plane_lsb(r1.x, e2, ma[4], mb[4], q, l);
-              cmp_plane_lsb(r0.w, e2, ma[3], mb[3], q, l);
-              cmp_plane_lsb(r0.z, e2, ma[2], mb[2], q, l);
-              cmp_plane_lsb(r0.y, e2, ma[1], mb[1], q, l);
-              cmp_plane_lsb(r0.x, e2, ma[0], mb[0], q, l);
-              eq[j] = q;
-              lt[j] = l & pend;
-            } else {
-              A[j] = c.k3 | c.k4;
-              wsum[j] = wpos[j];
+          for (int j = 0; j < WPT; j++) {
+            const int wi = j * NT + tid;
+            A[j] = c2[j] = eq[j] = lt[j] = 0;
+            wpos[j] = wsum[j] = 0;
+            if (j < WPT - 1 || own[j]) {
+              const uint4 ga = __ldg(&geo2[2 * (p * nw + wi)]);
+              const uint4 gb = __ldg(&geo2[2 * (p * nw + wi) + 1]);
+              const uint4 m = __ldg(&msk[p * nw + wi]);
+              const uint32_t same = oth_w[j];
+              const uint32_t sh = shifted_nb2(st, same, ga, gb);
+              const Classes c =
+                  classes_pad(cur_w[j], same, sh, word_at(st, ga.x), word_at(st, ga.y), m);
+              wpos[j] = 2 * __popc(c.k3) + 4 * __popc(c.k4);
+              if (SA) {
+                A[j] = c.ge2 & ga.w;
+                wsum[j] = wpos[j];  // minus the accepted Delta<0 flips at commit
+                const uint32_t e2 = c.km2 & me2, e4 = c.km4 & me4;
+                c2[j] = e2;
+                const P4 r0 =
+                    philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p), 1u}, key0, key1);
+                const P4 r1 =
+                    philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p + 1), 1u}, key0, key1);
+                cmp_planes<L>(r0, r1, e2, e2 | e4, K2, K4, eq[j], lt[j]);
+              } else {
+                A[j] = c.k3 | c.k4;
+                wsum[j] = wpos[j];
+              }
             }
           }
-        }
+        };
+        if (kZp >= 8 && zp == 8) pass1(std::integral_constant<int, 8>{});
+        else if (kZp >= 4 && zp == 4) pass1(std::integral_constant<int, 4>{});
+        else pass1(std::integral_constant<int, 0>{});
+
         // ---- pass 2 (SA): warp-cooperative tail.  Undecided sites take bits
         // 23..0 of their uniform from a per-site Philox word; the warp shares
         // out the words that hold undecided sites (items), 32 per round, and
@@ -696,6 +694,9 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.nbytes = (rows * cols + 7) / 8;
   a.err = err_ws;
   a.blocks = (unsigned long long *)((char *)err_ws + 8);
+  a.zp_max = 8;
+  if (const char *zv = getenv("GSB_CHECKER_ZP"))  // development A/B knob: 0, 4 or 8
+    a.zp_max = atoi(zv);
   const bool sa = kind == GSB_ANNEALING;
   // Team shape: W warps per trial (power of two), WPT <= 8 words per lane.
   // As few warps per trial as possible (a one-warp team needs no CTA barriers
