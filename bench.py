@@ -219,9 +219,12 @@ def main():
     share = os.environ.get("GSB_BENCH_SHARE_GPU") == "1"
     if share:
         local = 0
+    # under torchrun a process group always exists (also at world size 1, so
+    # the NCCL collectives of the reduction run on a one-GPU box too)
+    use_pg = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if use_pg:
         if share:
             dist.init_process_group("gloo")
         else:
@@ -283,7 +286,7 @@ def main():
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
-    if world > 1:
+    if use_pg:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -298,7 +301,7 @@ def main():
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         kern_ms.append(e0.elapsed_time(ek))
-    if world > 1:
+    if use_pg:
         dist.barrier()
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -307,7 +310,7 @@ def main():
 
     tot_ms = sum(step_ms)
     tot_kern = sum(kern_ms)
-    if world > 1:
+    if use_pg:
         t = torch.tensor([tot_ms, tot_kern], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms, tot_kern = float(t[0]), float(t[1])
@@ -332,7 +335,7 @@ def main():
                                               se_h.data_ptr(), bits_h.data_ptr(), sp))
 
         host_call()
-        if world > 1:
+        if use_pg:
             dist.barrier()
         e2e_s = []
         for _ in range(a.steps):
@@ -342,7 +345,7 @@ def main():
             host_call()
             e2e_s.append(time.perf_counter() - t0)
         tot_e2e = sum(e2e_s)
-        if world > 1:
+        if use_pg:
             t = torch.tensor([tot_e2e], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot_e2e = float(t[0])
@@ -464,7 +467,7 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_pg:
         dist.destroy_process_group()
     return 0
 

@@ -67,7 +67,10 @@ def reduce_best(local_cut, local_bits, first_index: int, num_trials: int, group=
     import torch
     import torch.distributed as dist
 
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    # collectives run whenever a process group exists (also at world size 1,
+    # so a one-GPU NCCL group exercises the same calls as eight GPUs)
+    pg = dist.is_initialized()
+    world = dist.get_world_size(group) if pg else 1
     dev = local_cut.device
     nbytes = local_bits.shape[1]
     if local_cut.numel():
@@ -86,17 +89,18 @@ def reduce_best(local_cut, local_bits, first_index: int, num_trials: int, group=
         k = keys.max().reshape(1)
     else:
         k = torch.full((1,), torch.iinfo(torch.int64).min, device=dev, dtype=torch.int64)
-    if world > 1:
+    if pg:
         dist.all_reduce(k, op=dist.ReduceOp.MAX, group=group)
     gk = int(k.item())
     cut, index = decode_key(gk)
     bits = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    owner = owner_of(index, num_trials, world) if world > 1 else 0
-    rank = dist.get_rank(group) if world > 1 else 0
+    owner = owner_of(index, num_trials, world)
+    rank = dist.get_rank(group) if pg else 0
     if rank == owner:
         bits.copy_(local_bits[index - first_index])
-    if world > 1:
-        dist.broadcast(bits, src=owner, group=group)
+    if pg:
+        dist.broadcast(bits, src=dist.get_global_rank(group, owner) if group is not None else owner,
+                       group=group)
     return GlobalBest(best_cut=cut, index=index, bits=bits.cpu().numpy())
 
 
@@ -105,9 +109,9 @@ def gather_trials(local_cut, local_sweeps, num_trials: int, group=None):
     import torch
     import torch.distributed as dist
 
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    if world == 1:
+    if not dist.is_initialized():
         return local_cut.cpu().numpy(), local_sweeps.cpu().numpy()
+    world = dist.get_world_size(group)
     dev = local_cut.device
     maxc = -(-num_trials // world)
     pc = torch.zeros(maxc, dtype=torch.int64, device=dev)
