@@ -55,6 +55,10 @@ extern "C" {
 #define GSB_ENGINE_CHECKERBOARD_CLUSTER 3 /* same contract, forces the cluster engine (one trial
                                              over the shared memory of a CTA cluster; used
                                              automatically when the torus exceeds one SM) */
+#define GSB_ENGINE_RANDOM_SCAN 4  /* Philox4x32-10 + the reference's random visit order, drawn
+                                     as priorities and run level by level (DESIGN.md random-scan
+                                     contract): the reference's dynamics in law; any torus
+                                     that fits one SM */
 
 typedef struct gsb_torus {
     int32_t rows, cols;  /* TorusSpec.rows/cols (instances.py:186-187), >= 3 */

@@ -495,6 +495,136 @@ static int trial_checker(int32_t rows, int32_t cols, const int8_t *w, const int3
     return rc;
 }
 
+/* ------------------------------------------------------------------ */
+/* random-scan (Philox) trial -- DESIGN.md "Random-scan contract"       */
+/* ------------------------------------------------------------------ */
+/* The reference's sweep visits the sites in a fresh uniformly random order
+ * (solvers.py:110).  Here the order of sweep t is that of the priorities
+ *   p(v) = word (v & 3) of Philox(key, (v >> 2, t, 0, 4)), ties by v,
+ * executed level by level: lvl(v) = 1 + max lvl(u) over the neighbours u that
+ * precede v (0 if none), visit order (lvl, v).  Every order with each site
+ * after its preceding neighbours gives the same spins after each site's visit,
+ * so the states at level boundaries and at the end of the sweep are those of
+ * the sequential scan in priority order: the reference's dynamics in law, with
+ * Philox instead of PCG64.  Other draws:
+ *   initial spin of v: top bit of word (v & 3) of Philox(key, (v >> 2, 0, 0, 3));
+ *   uniform of v at sweep t: word (v & 3) of Philox(key, (v >> 2, t, 1, 4)),
+ *   accept Delta < 0 iff u * 2^-32 < exp(Delta / T_t). */
+typedef struct {
+    uint32_t p;
+    int32_t v;
+} prio_t;
+
+static int prio_cmp(const void *a, const void *b) {
+    const prio_t *x = (const prio_t *)a, *y = (const prio_t *)b;
+    if (x->p != y->p) return x->p < y->p ? -1 : 1;
+    return x->v < y->v ? -1 : (x->v > y->v);
+}
+
+static uint32_t philox_word(const uint32_t key[2], uint32_t c0, uint32_t c1, uint32_t c2,
+                            uint32_t c3, int word) {
+    uint32_t ctr[4] = {c0, c1, c2, c3}, o[4];
+    gso_philox4x32_10(ctr, key, o);
+    return o[word];
+}
+
+static int trial_rscan(int32_t rows, int32_t cols, const int8_t *w, const int32_t *eu,
+                       const int32_t *ev, const int64_t *ew, int kind, int32_t sweeps,
+                       uint64_t seed, double t0, double t1, int64_t *best_cut,
+                       int8_t *best_spins, int32_t *sweeps_executed) {
+    int32_t n = rows * cols;
+    int64_t m = 2 * (int64_t)n;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    int8_t *s = (int8_t *)malloc((size_t)n);
+    int8_t *bs = (int8_t *)malloc((size_t)n);
+    prio_t *pr = (prio_t *)malloc(sizeof(prio_t) * (size_t)n);
+    uint32_t *pv = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n);
+    int32_t *lvl = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *cnt = (int32_t *)malloc(sizeof(int32_t) * ((size_t)n + 2));
+    int32_t *flog = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    for (int32_t v = 0; v < n; v++)
+        s[v] = (philox_word(key, (uint32_t)(v >> 2), 0u, 0u, 3u, v & 3) >> 31) ? 1 : -1;
+    int64_t current = gso_cut(m, eu, ev, ew, s);
+    int64_t best = current;
+    memcpy(bs, s, (size_t)n);
+    int32_t executed = 0;
+    int annealing = kind == GSO_ANNEALING;
+    for (int32_t sweep = 0; sweep < sweeps; sweep++) {
+        double temp = annealing ? gso_temperature(sweeps, t0, t1, sweep) : 0.0;
+        /* priorities, levels (sequential in priority order), visit order */
+        for (int32_t v = 0; v < n; v++) {
+            pv[v] = philox_word(key, (uint32_t)(v >> 2), (uint32_t)sweep, 0u, 4u, v & 3);
+            pr[v].p = pv[v];
+            pr[v].v = v;
+        }
+        qsort(pr, (size_t)n, sizeof(prio_t), prio_cmp);
+        int32_t maxl = 0;
+        for (int32_t i = 0; i < n; i++) {
+            int32_t v = pr[i].v, r = v / cols, c = v % cols;
+            int32_t nb[4] = {((r + rows - 1) % rows) * cols + c, ((r + 1) % rows) * cols + c,
+                             r * cols + (c + cols - 1) % cols, r * cols + (c + 1) % cols};
+            int32_t L = 0;
+            for (int d = 0; d < 4; d++) {
+                int32_t u = nb[d];
+                if (pv[u] < pv[v] || (pv[u] == pv[v] && u < v))
+                    if (lvl[u] > L) L = lvl[u];
+            }
+            lvl[v] = L + 1;
+            if (L + 1 > maxl) maxl = L + 1;
+        }
+        for (int32_t l = 0; l <= maxl + 1; l++) cnt[l] = 0;
+        for (int32_t v = 0; v < n; v++) cnt[lvl[v] + 1]++;
+        for (int32_t l = 1; l <= maxl + 1; l++) cnt[l] += cnt[l - 1];
+        for (int32_t v = 0; v < n; v++) order[cnt[lvl[v]]++] = v; /* (lvl, v) */
+        int flipped = 0;
+        int64_t nlog = 0, nbest = -1;
+        for (int32_t i = 0; i < n; i++) {
+            int32_t v = order[i], r = v / cols, c = v % cols;
+            int32_t cl = (c + cols - 1) % cols, cr = (c + 1) % cols;
+            int32_t ru = (r + rows - 1) % rows, rd = (r + 1) % rows;
+            int64_t delta = (int64_t)w[2 * v] * s[r * cols + cr] +
+                            (int64_t)w[2 * v + 1] * s[rd * cols + c] +
+                            (int64_t)w[2 * (r * cols + cl)] * s[r * cols + cl] +
+                            (int64_t)w[2 * (ru * cols + c) + 1] * s[ru * cols + c];
+            delta *= s[v];
+            int accept;
+            if (annealing) {
+                accept = delta >= 0;
+                if (!accept) {
+                    uint32_t u = philox_word(key, (uint32_t)(v >> 2), (uint32_t)sweep, 1u, 4u, v & 3);
+                    accept = (double)u * (1.0 / 4294967296.0) < exp((double)delta / temp);
+                }
+            } else {
+                accept = delta > 0;
+            }
+            if (accept) {
+                s[v] = (int8_t)-s[v];
+                current += delta;
+                flipped = 1;
+                flog[nlog++] = v;
+                if (current > best) {
+                    best = current;
+                    nbest = nlog;
+                }
+            }
+        }
+        if (nbest >= 0) { /* snapshot at the last improvement of the sweep */
+            memcpy(bs, s, (size_t)n);
+            for (int64_t f = nbest; f < nlog; f++) bs[flog[f]] = (int8_t)-bs[flog[f]];
+        }
+        executed = sweep + 1;
+        if (!annealing && !flipped) break;
+    }
+    int rc = 0;
+    if (best != gso_cut(m, eu, ev, ew, bs)) rc = -1;
+    *best_cut = best;
+    if (best_spins) memcpy(best_spins, bs, (size_t)n);
+    *sweeps_executed = executed;
+    free(s); free(bs); free(pr); free(pv); free(lvl); free(order); free(cnt); free(flog);
+    return rc;
+}
+
 typedef struct {
     int32_t rows, cols;
     const int8_t *w;
@@ -533,11 +663,22 @@ int gso_run_trial_checker(int32_t rows, int32_t cols, const int8_t *w, int kind,
     return rc;
 }
 
+int gso_run_trial_rscan(int32_t rows, int32_t cols, const int8_t *w, int kind, int32_t sweeps,
+                        uint64_t seed, double t0, double t1, int64_t *best_cut,
+                        int8_t *best_spins, int32_t *sweeps_executed) {
+    torus_edges_t te;
+    if (torus_edges_alloc(&te, rows, cols, w)) return -2;
+    int rc = trial_rscan(rows, cols, w, te.eu, te.ev, te.ew, kind, sweeps, seed, t0, t1,
+                         best_cut, best_spins, sweeps_executed);
+    torus_edges_free(&te);
+    return rc;
+}
+
 /* ------------------------------------------------------------------ */
 /* batched, multi-threaded                                              */
 /* ------------------------------------------------------------------ */
 typedef struct {
-    int mode; /* 0 ref, 1 checker */
+    int mode; /* 0 ref, 1 checker, 2 random scan */
     const csr_t *G;
     int64_t m;
     const int32_t *eu, *ev;
@@ -564,10 +705,14 @@ static void *job_run(void *arg) {
         if (j->mode == 0)
             rc = trial_ref_csr(j->G, j->m, j->eu, j->ev, j->ew, j->kind, j->sweeps, j->seeds[t],
                                j->t0, j->t1, &j->best_cut[t], bs, &j->sweeps_executed[t]);
-        else
+        else if (j->mode == 1)
             rc = trial_checker(j->rows, j->cols, j->w, j->eu, j->ev, j->ew, j->kind, j->sweeps,
                                j->seeds[t], j->t0, j->t1, &j->best_cut[t], bs,
                                &j->sweeps_executed[t]);
+        else
+            rc = trial_rscan(j->rows, j->cols, j->w, j->eu, j->ev, j->ew, j->kind, j->sweeps,
+                             j->seeds[t], j->t0, j->t1, &j->best_cut[t], bs,
+                             &j->sweeps_executed[t]);
         if (rc && !j->rc) j->rc = rc;
     }
     return NULL;
@@ -623,15 +768,15 @@ int gso_run_trials_ref(int32_t n, int64_t m, const int32_t *eu, const int32_t *e
     return rc;
 }
 
-int gso_run_trials_checker(int32_t rows, int32_t cols, const int8_t *w, int kind,
-                           int32_t sweeps, int32_t T, const uint64_t *seeds, double t0,
-                           double t1, int64_t *best_cut, int8_t *best_spins,
-                           int32_t *sweeps_executed, int nthreads) {
+static int run_torus_jobs(int mode, int32_t rows, int32_t cols, const int8_t *w, int kind,
+                          int32_t sweeps, int32_t T, const uint64_t *seeds, double t0,
+                          double t1, int64_t *best_cut, int8_t *best_spins,
+                          int32_t *sweeps_executed, int nthreads) {
     torus_edges_t te;
     if (torus_edges_alloc(&te, rows, cols, w)) return -2;
     job_t p;
     memset(&p, 0, sizeof p);
-    p.mode = 1;
+    p.mode = mode;
     p.m = te.m;
     p.eu = te.eu;
     p.ev = te.ev;
@@ -652,4 +797,20 @@ int gso_run_trials_checker(int32_t rows, int32_t cols, const int8_t *w, int kind
     int rc = run_jobs(&p, nthreads);
     torus_edges_free(&te);
     return rc;
+}
+
+int gso_run_trials_checker(int32_t rows, int32_t cols, const int8_t *w, int kind,
+                           int32_t sweeps, int32_t T, const uint64_t *seeds, double t0,
+                           double t1, int64_t *best_cut, int8_t *best_spins,
+                           int32_t *sweeps_executed, int nthreads) {
+    return run_torus_jobs(1, rows, cols, w, kind, sweeps, T, seeds, t0, t1, best_cut, best_spins,
+                          sweeps_executed, nthreads);
+}
+
+int gso_run_trials_rscan(int32_t rows, int32_t cols, const int8_t *w, int kind, int32_t sweeps,
+                         int32_t T, const uint64_t *seeds, double t0, double t1,
+                         int64_t *best_cut, int8_t *best_spins, int32_t *sweeps_executed,
+                         int nthreads) {
+    return run_torus_jobs(2, rows, cols, w, kind, sweeps, T, seeds, t0, t1, best_cut, best_spins,
+                          sweeps_executed, nthreads);
 }

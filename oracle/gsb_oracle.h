@@ -23,6 +23,10 @@
  *      then all colour-1 sites) and the RNG (counter-based Philox4x32-10 keyed by
  *      the trial seed).  DESIGN.md section "Checkerboard contract" is the
  *      normative statement; this file is its executable form.
+ *
+ *  (3) "random scan" (Philox): the reference's random-order sweep, the order
+ *      drawn as Philox priorities and executed level by level -- the
+ *      reference's dynamics in law.
  */
 #ifndef GSB_ORACLE_H
 #define GSB_ORACLE_H
@@ -83,6 +87,13 @@ int gso_run_trial_checker(int32_t rows, int32_t cols, const int8_t *w, int kind,
                           int32_t sweeps, uint64_t seed, double t0, double t1,
                           int64_t *best_cut, int8_t *best_spins, int32_t *sweeps_executed);
 
+/* random-scan (Philox) trial on any rows x cols torus (rows, cols >= 3): the
+ * reference's random-order sweep with priorities drawn from Philox, executed
+ * level by level. */
+int gso_run_trial_rscan(int32_t rows, int32_t cols, const int8_t *w, int kind, int32_t sweeps,
+                        uint64_t seed, double t0, double t1, int64_t *best_cut,
+                        int8_t *best_spins, int32_t *sweeps_executed);
+
 /* batched, multi-threaded (pthreads) versions: trial t uses seeds[t];
  * best_spins is [T][n] (may be NULL).  Returns 0 or the first failure. */
 int gso_run_trials_ref(int32_t n, int64_t m, const int32_t *eu, const int32_t *ev,
@@ -93,6 +104,10 @@ int gso_run_trials_checker(int32_t rows, int32_t cols, const int8_t *w, int kind
                            int32_t sweeps, int32_t T, const uint64_t *seeds, double t0,
                            double t1, int64_t *best_cut, int8_t *best_spins,
                            int32_t *sweeps_executed, int nthreads);
+int gso_run_trials_rscan(int32_t rows, int32_t cols, const int8_t *w, int kind, int32_t sweeps,
+                         int32_t T, const uint64_t *seeds, double t0, double t1,
+                         int64_t *best_cut, int8_t *best_spins, int32_t *sweeps_executed,
+                         int nthreads);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,8 @@ LIB = HERE / "build" / "libgsb_oracle.so"
 
 GREEDY, ANNEALING = 0, 1
 _KIND = {"greedy_local_search": GREEDY, "simulated_annealing": ANNEALING,
-         "greedy_checkerboard": GREEDY, "simulated_annealing_checkerboard": ANNEALING}
+         "greedy_checkerboard": GREEDY, "simulated_annealing_checkerboard": ANNEALING,
+         "greedy_random_scan": GREEDY, "simulated_annealing_random_scan": ANNEALING}
 
 _lib = None
 
@@ -65,6 +66,8 @@ def lib():
         L.gso_philox4x32_10.argtypes = [P, P, P]
         L.gso_run_trials_ref.argtypes = [i32, i64, P, P, P, ctypes.c_int, i32, i32, P, dbl, dbl,
                                          P, P, P, ctypes.c_int]
+        L.gso_run_trials_rscan.argtypes = [i32, i32, P, ctypes.c_int, i32, i32, P, dbl, dbl,
+                                           P, P, P, ctypes.c_int]
         L.gso_run_trials_checker.argtypes = [i32, i32, P, ctypes.c_int, i32, i32, P, dbl, dbl,
                                              P, P, P, ctypes.c_int]
         _lib = L
@@ -178,6 +181,25 @@ def run_trials_checker(rows, cols, w, kind, sweeps, seeds, t0=0.0, t1=0.0, spins
                                       _p(seeds), t0 or 0.0, t1 or 0.0, _p(bc),
                                       _p(bs) if spins else None, _p(se),
                                       nthreads or os.cpu_count())
+    if rc:
+        raise RuntimeError(f"oracle failed rc={rc}")
+    return bc, bs, se
+
+
+def run_trials_rscan(rows, cols, w, kind, sweeps, seeds, t0=0.0, t1=0.0, spins=True,
+                     nthreads=None):
+    """Random-scan/Philox trials on a torus (DESIGN.md random-scan contract)."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    T = len(seeds)
+    n = rows * cols
+    bc = np.empty(T, np.int64)
+    se = np.empty(T, np.int32)
+    bs = np.empty((T, n), np.int8) if spins else None
+    w = np.ascontiguousarray(w, np.int8)
+    rc = lib().gso_run_trials_rscan(rows, cols, _p(w), _KIND.get(kind, kind), sweeps, T,
+                                    _p(seeds), t0 or 0.0, t1 or 0.0, _p(bc),
+                                    _p(bs) if spins else None, _p(se),
+                                    nthreads or os.cpu_count())
     if rc:
         raise RuntimeError(f"oracle failed rc={rc}")
     return bc, bs, se

@@ -27,6 +27,7 @@ ENGINE_REFERENCE = 0
 ENGINE_CHECKERBOARD = 1
 ENGINE_CHECKERBOARD_TILED = 2
 ENGINE_CHECKERBOARD_CLUSTER = 3
+ENGINE_RANDOM_SCAN = 4
 
 _lock = threading.Lock()
 _lib = None

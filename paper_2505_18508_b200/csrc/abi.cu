@@ -132,7 +132,7 @@ int gsb_schedule_table(int engine, int32_t sweeps, double t0, double t1, int32_t
   if (engine == GSB_ENGINE_REFERENCE)
     bits = 53;
   else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
-           engine == GSB_ENGINE_CHECKERBOARD_CLUSTER)
+           engine == GSB_ENGINE_CHECKERBOARD_CLUSTER || engine == GSB_ENGINE_RANDOM_SCAN)
     bits = 32;
   else
     return set_error(GSB_EINVAL, "unknown engine");
@@ -153,7 +153,9 @@ size_t gsb_torus_workspace_bytes(const gsb_torus *inst, int engine, int32_t swee
   if (!inst) return 0;
   int n = inst->rows * inst->cols;
   size_t b = err_bytes();
-  if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
+  if (engine == GSB_ENGINE_RANDOM_SCAN) {
+    // no scratch beyond the error word and counters
+  } else if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
     b += checker_workspace_bytes(inst->rows, inst->cols);
   } else if ((engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_CLUSTER) &&
              checker_cluster_fits(inst->rows, inst->cols)) {
@@ -218,6 +220,9 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     } else {
       return set_error(GSB_EUNSUPPORTED, "torus too large for the checkerboard engines");
     }
+  } else if (engine == GSB_ENGINE_RANDOM_SCAN) {
+    rc = rscan_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
+                   sweeps_exec, best_bits, err, stream);
   } else if (engine == GSB_ENGINE_REFERENCE && ref_warp_fits(inst->rows, inst->cols)) {
     rc = ref_warp_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
                       sweeps_exec, best_bits, rest, err, stream);

@@ -173,3 +173,96 @@ def test_checker_oracle_statistically_matches_reference(oracle):
                                          3.0, 0.05, spins=False)
     assert int((bc >= 10).sum()) >= 80
     assert int(bc.max()) == 10
+
+
+def test_random_scan_contract_agrees_in_law_with_reference(oracle):
+    """The random-scan contract (priorities from Philox, level-by-level order)
+    against the reference-exact oracle (pinned to the Python reference above):
+    same torus, schedule and seeds, final-cut distributions agree (KS p > 1e-3,
+    means within 4 standard errors); the checkerboard order does not."""
+    stats = pytest.importorskip("scipy.stats")
+    from paper_2505_18508_b200.campaign import mix_seeds
+
+    R, C, T, S = 20, 30, 768, 150
+    w = oracle.torus_weights(R, C, 1)
+    eu, ev, ew = oracle.torus_edges(R, C, w)
+    seeds = mix_seeds(20250814, range(T))
+    a = oracle.run_trials_ref(R * C, eu, ev, ew, "simulated_annealing", S, seeds, 3.0, 0.05,
+                              spins=False)[0].astype(float)
+    b = oracle.run_trials_rscan(R, C, w, "simulated_annealing_random_scan", S, seeds, 3.0, 0.05,
+                                spins=False)[0].astype(float)
+    c = oracle.run_trials_checker(R, C, w, "simulated_annealing_checkerboard", S, seeds, 3.0,
+                                  0.05, spins=False)[0].astype(float)
+    se = np.sqrt(a.var(ddof=1) / T + b.var(ddof=1) / T)
+    assert abs(a.mean() - b.mean()) < 4 * se
+    assert stats.ks_2samp(a, b).pvalue > 1e-3
+    assert c.mean() - a.mean() > 4 * se
+
+
+def test_random_scan_oracle_matches_python_restatement(oracle):
+    """Pure-Python restatement of the random-scan contract on small tori: the
+    oracle's (best_cut, best spins) equal it, and every sweep's level-by-level
+    order leaves the same spins as the sequential scan in priority order (the
+    identity the contract rests on)."""
+    import math
+
+    from paper_2505_18508_b200.campaign import mix_seeds
+
+    for (R, C, s) in [(3, 3, 1), (4, 5, 2), (6, 7, 3)]:
+        w = [int(x) for x in oracle.torus_weights(R, C, s)]
+        n = R * C
+        nbrs = []
+        for v in range(n):
+            r, c = divmod(v, C)
+            nbrs.append((((r - 1) % R) * C + c, ((r + 1) % R) * C + c, r * C + (c - 1) % C,
+                         r * C + (c + 1) % C))
+
+        def delta(v, sp):
+            up, dn, lf, rt = nbrs[v]
+            return sp[v] * (w[2 * v] * sp[rt] + w[2 * v + 1] * sp[dn] + w[2 * lf] * sp[lf] +
+                            w[2 * up + 1] * sp[up])
+
+        def cut(sp):
+            return sum(w[2 * v] * (sp[v] != sp[nbrs[v][3]]) + w[2 * v + 1] * (sp[v] != sp[nbrs[v][1]])
+                       for v in range(n))
+
+        for seed in mix_seeds(7, range(3)):
+            seed = int(seed)
+            key = [seed & 0xFFFFFFFF, seed >> 32]
+
+            def ph(q, t, a, b, i):
+                return oracle.philox([q, t, a, b], key)[i]
+
+            sp = [1 if ph(v >> 2, 0, 0, 3, v & 3) >> 31 else -1 for v in range(n)]
+            S, t0, t1 = 6, 3.0, 0.05
+            cur = best = cut(sp)
+            bsp = list(sp)
+            for t in range(S):
+                T = t0 * (t1 / t0) ** (t / (S - 1))
+                pr = [ph(v >> 2, t, 0, 4, v & 3) for v in range(n)]
+                u = [ph(v >> 2, t, 1, 4, v & 3) for v in range(n)]
+
+                def visit(v, st):
+                    d = delta(v, st)
+                    if d >= 0 or u[v] / 2**32 < math.exp(d / T):
+                        st[v] = -st[v]
+                        return d
+                    return None
+
+                seq = list(sp)
+                by_prio = sorted(range(n), key=lambda v: (pr[v], v))
+                for v in by_prio:
+                    visit(v, seq)
+                lvl = [0] * n
+                for v in by_prio:
+                    lvl[v] = 1 + max([lvl[x] for x in nbrs[v] if (pr[x], x) < (pr[v], v)] or [0])
+                for v in sorted(range(n), key=lambda v: (lvl[v], v)):
+                    d = visit(v, sp)
+                    if d is not None:
+                        cur += d
+                        if cur > best:
+                            best, bsp = cur, list(sp)
+                assert sp == seq, (R, C, seed, t)
+            bc, bs, _ = oracle.run_trials_rscan(R, C, oracle.torus_weights(R, C, s),
+                                                "simulated_annealing_random_scan", S, [seed], t0, t1)
+            assert int(bc[0]) == best and [int(x) for x in bs[0]] == bsp, (R, C, seed)
