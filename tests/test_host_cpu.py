@@ -61,7 +61,8 @@ def test_config_validation():  # test_solvers.py:18-30
         SolverConfig(kind=GREEDY, sweeps=1, seed=0, temp_start=1.0)
     with pytest.raises(ValueError, match="temp_start"):
         SolverConfig(kind=ANNEALING_CHECKERBOARD, sweeps=1, seed=0)
-    assert set(KINDS) == {GREEDY, ANNEALING, GREEDY_CHECKERBOARD, ANNEALING_CHECKERBOARD}
+    assert set(KINDS) == {GREEDY, ANNEALING, GREEDY_CHECKERBOARD, ANNEALING_CHECKERBOARD,
+                          "greedy_random_scan", "simulated_annealing_random_scan"}
 
 
 def test_default_config_and_schedule():  # test_solvers.py:33-46
