@@ -63,21 +63,30 @@ __device__ __forceinline__ long long rs_warp_max_key(long long key) {
   return (long long)(((unsigned long long)(unsigned)mh << 32) | ml);
 }
 
+// Per-site meta byte: preceding-neighbour mask (bits 0-3: up, down, left,
+// right), right / down coupling is -1 (bits 4 / 5), spin is +1 (bit 6).
+constexpr uint32_t RS_WR = 16, RS_WD = 32, RS_SP = 64;
+
 template <int KW, bool SA>
-__global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
-  constexpr int K = 32 * KW;
+__global__ void __launch_bounds__(RS_MAXNT, 2) rscan_kernel(RsArgs a) {
+  constexpr int K = 32 * KW;                 // sites per thread
+  constexpr int LK = KW == 1 ? 5 : KW == 2 ? 6 : 7;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ RsShared sh;
   const int n = a.n, npad = a.npad, cols = a.cols, rows = a.rows;
-  uint32_t *pu = (uint32_t *)smem_raw;           // [npad] priorities, then uniforms
-  uint32_t *bst = pu + npad;                     // [npad / 32] best snapshot bits
-  uint32_t *cnt = bst + npad / 32;               // [npad / 8] 4-bit counts of unvisited preceding neighbours
-  int8_t *s = (int8_t *)(cnt + npad / 8);        // [npad] spins +-1
-  uint8_t *em = (uint8_t *)(s + npad);           // [npad] preceding neighbours: up 1 down 2 left 4 right 8
-  int8_t *dl = (int8_t *)(em + npad);            // [npad] accepted Delta of the round
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+  const int NT = blockDim.x;
+  // Shared arrays are transposed: site v (owner v >> LK, offset o = v & (K-1))
+  // lives at o * NT + owner, so the lanes of a warp touching the same offset
+  // of their own sites hit consecutive addresses (no bank conflicts).
+  uint32_t *pu = (uint32_t *)smem_raw;        // [npad] priorities, then uniforms
+  uint32_t *bst = pu + npad;                  // [KW][NT] best snapshot bits (bit b of word j: offset 32j+b)
+  uint32_t *cnt = bst + npad / 32;            // [K/8][NT] 4-bit wait counts, 8 offsets per word
+  uint8_t *meta = (uint8_t *)(cnt + npad / 8);  // [npad]
+  int8_t *dl = (int8_t *)(meta + npad);       // [npad] accepted Delta of the round
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = NT >> 5;
   const int v0 = tid * K;
 
+  auto tix = [&](int v) { return (v & (K - 1)) * NT + (v >> LK); };
   auto nbr = [&](int v, int &up, int &dn, int &lf, int &rt) {
     const int r = (int)__umulhi((uint32_t)v, a.rdiv), c = v - r * cols;
     up = (r == 0 ? rows - 1 : r - 1) * cols + c;
@@ -85,7 +94,6 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
     lf = r * cols + (c == 0 ? cols - 1 : c - 1);
     rt = r * cols + (c == cols - 1 ? 0 : c + 1);
   };
-  // block sum of x (all threads get it); uses sh.scan, two barriers
   auto block_sum = [&](int x) {
     x = (int)__reduce_add_sync(0xffffffffu, (unsigned)x);
     if (lane == 0) sh.scan[warp] = x;
@@ -95,42 +103,62 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
     __syncthreads();
     return t;
   };
-  // cut contribution of own sites' right and down edges, spins from `get`
+  // cut of own sites' right and down edges; spin(v) in {0, 1} from `get`
   auto own_cut = [&](auto get) {
     int c0 = 0;
-    for (int i = 0; i < K; i++) {
-      const int v = v0 + i;
+    for (int o = 0; o < K; o++) {
+      const int v = v0 + o;
       if (v >= n) break;
       int up, dn, lf, rt;
       nbr(v, up, dn, lf, rt);
-      const int sv = get(v);
-      if (sv != get(rt)) c0 += __ldg(&a.w[2 * v]);
-      if (sv != get(dn)) c0 += __ldg(&a.w[2 * v + 1]);
+      const uint32_t m = meta[o * NT + tid];
+      const uint32_t sv = get(v);
+      if (sv != get(rt)) c0 += (m & RS_WR) ? -1 : 1;
+      if (sv != get(dn)) c0 += (m & RS_WD) ? -1 : 1;
     }
     return c0;
   };
+  auto bst_bit = [&](int v) -> uint32_t {
+    const int o = v & (K - 1);
+    return (bst[(o >> 5) * NT + (v >> LK)] >> (o & 31)) & 1u;
+  };
+
+  // coupling bits of the own sites (same for every trial)
+  for (int o = 0; o < K; o++) {
+    const int v = v0 + o;
+    uint32_t m = 0;
+    if (v < n) {
+      if (a.w[2 * v] < 0) m |= RS_WR;
+      if (a.w[2 * v + 1] < 0) m |= RS_WD;
+    }
+    meta[o * NT + tid] = (uint8_t)m;
+  }
 
   unsigned long long nblocks = 0;
   for (int trial = blockIdx.x; trial < a.T; trial += gridDim.x) {
     const uint64_t seed = a.seeds[trial];
     const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
     // ---- initial spins: top bit of word (v & 3) of Philox(key, (v >> 2, 0, 0, 3))
+    uint32_t sb[KW];  // own spins, bit o & 31 of word o >> 5 (1 = +1)
+#pragma unroll
+    for (int j = 0; j < KW; j++) sb[j] = 0;
 #pragma unroll 4
     for (int i = 0; i < K / 4; i++) {
-      const int q = (v0 >> 2) + i;
-      const P4 o = philox10(P4{(uint32_t)q, 0u, 0u, 3u}, key0, key1);
-      nblocks++;
-      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+      const P4 o4 = philox10(P4{(uint32_t)((v0 >> 2) + i), 0u, 0u, 3u}, key0, key1);
+      const uint32_t nib = (o4.x >> 31) | ((o4.y >> 31) << 1) | ((o4.z >> 31) << 2) | ((o4.w >> 31) << 3);
 #pragma unroll
-      for (int i = 0; i < 4; i++) s[4 * q + i] = (ow[i] >> 31) ? 1 : -1;
+      for (int j = 0; j < KW; j++)
+        if ((i >> 3) == j) sb[j] |= nib << (4 * (i & 7));
     }
-    for (int j = 0; j < KW; j++) {  // snapshot = initial spins (bit = +1)
-      uint32_t b = 0;
-      for (int i = 0; i < 32; i++) b |= (s[v0 + 32 * j + i] > 0 ? 1u : 0u) << i;
-      bst[tid * KW + j] = b;
+    nblocks += K / 4;
+    for (int o = 0; o < K; o++) {
+      const uint32_t bit = (sb[o >> 5] >> (o & 31)) & 1u;
+      meta[o * NT + tid] = (uint8_t)((meta[o * NT + tid] & (RS_WR | RS_WD)) | (bit ? RS_SP : 0u));
     }
+#pragma unroll
+    for (int j = 0; j < KW; j++) bst[j * NT + tid] = sb[j];
     __syncthreads();
-    int cur = block_sum(own_cut([&](int v) { return (int)s[v]; }));
+    int cur = block_sum(own_cut([&](int v) { return (uint32_t)(meta[tix(v)] >> 6) & 1u; }));
     int best = cur;
     int executed = 0;
 
@@ -140,60 +168,63 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
         Kd2 = a.table[(size_t)t * 4 + 1];
         Kd4 = a.table[(size_t)t * 4 + 3];
       }
-      // ---- priorities of the sweep (K / 4 independent Philox blocks)
+      // ---- priorities of the sweep
 #pragma unroll 4
       for (int i = 0; i < K / 4; i++) {
-        const int q = (v0 >> 2) + i;
-        const P4 o = philox10(P4{(uint32_t)q, (uint32_t)t, 0u, 4u}, key0, key1);
-        *(uint4 *)&pu[4 * q] = make_uint4(o.x, o.y, o.z, o.w);
+        const P4 o4 = philox10(P4{(uint32_t)((v0 >> 2) + i), (uint32_t)t, 0u, 4u}, key0, key1);
+        pu[(4 * i) * NT + tid] = o4.x;
+        pu[(4 * i + 1) * NT + tid] = o4.y;
+        pu[(4 * i + 2) * NT + tid] = o4.z;
+        pu[(4 * i + 3) * NT + tid] = o4.w;
       }
       nblocks += K / 4;
       __syncthreads();
       // ---- preceding neighbours (p(u), u) < (p(v), v) and the wait counts
-      // (4 bits per site, 8 sites per word, all words owned by this thread)
       uint32_t todo[KW];
 #pragma unroll
-      for (int j = 0; j < KW; j++) {
-        todo[j] = 0;
+      for (int j = 0; j < KW; j++) todo[j] = 0;
 #pragma unroll 1
-        for (int b8 = 0; b8 < 4; b8++) {
-          uint32_t cw = 0;
+      for (int o8 = 0; o8 < K / 8; o8++) {
+        uint32_t cw = 0;
+#pragma unroll 2
+        for (int b = 0; b < 8; b++) {
+          const int o = 8 * o8 + b, v = v0 + o;
+          if (v < n) {
+            int nb[4];
+            nbr(v, nb[0], nb[1], nb[2], nb[3]);
+            const uint32_t pv = pu[o * NT + tid];
+            uint32_t m = 0;
 #pragma unroll
-          for (int b = 8 * b8; b < 8 * b8 + 8; b++) {
-            const int v = v0 + 32 * j + b;
-            if (v < n) {
-              int nb[4];
-              nbr(v, nb[0], nb[1], nb[2], nb[3]);
-              const uint32_t pv = pu[v];
-              uint32_t m = 0;
-#pragma unroll
-              for (int d = 0; d < 4; d++) {
-                const uint32_t pn = pu[nb[d]];
-                if (pn < pv || (pn == pv && nb[d] < v)) m |= 1u << d;
-              }
-              em[v] = (uint8_t)m;
-              todo[j] |= 1u << b;
-              cw |= (uint32_t)__popc(m) << (4 * (b & 7));
+            for (int d = 0; d < 4; d++) {
+              const uint32_t pn = pu[tix(nb[d])];
+              if (pn < pv || (pn == pv && nb[d] < v)) m |= 1u << d;
             }
+            meta[o * NT + tid] = (uint8_t)((meta[o * NT + tid] & 0xF0u) | m);
+            cw |= (uint32_t)__popc(m) << (4 * b);
+#pragma unroll
+            for (int j = 0; j < KW; j++)
+              if ((o >> 5) == j) todo[j] |= 1u << (o & 31);
           }
-          cnt[(v0 >> 3) + 4 * j + b8] = cw;
         }
+        cnt[o8 * NT + tid] = cw;
       }
       __syncthreads();  // every priority read before the slots take the uniforms
       if (SA) {
 #pragma unroll 4
         for (int i = 0; i < K / 4; i++) {
-          const int q = (v0 >> 2) + i;
-          const P4 o = philox10(P4{(uint32_t)q, (uint32_t)t, 1u, 4u}, key0, key1);
-          *(uint4 *)&pu[4 * q] = make_uint4(o.x, o.y, o.z, o.w);
+          const P4 o4 = philox10(P4{(uint32_t)((v0 >> 2) + i), (uint32_t)t, 1u, 4u}, key0, key1);
+          pu[(4 * i) * NT + tid] = o4.x;
+          pu[(4 * i + 1) * NT + tid] = o4.y;
+          pu[(4 * i + 2) * NT + tid] = o4.z;
+          pu[(4 * i + 3) * NT + tid] = o4.w;
         }
         nblocks += K / 4;
       }
       bool sweep_flipped = false;
-      // ---- rounds: a site is ready once its wait count is 0.  Each round:
-      // the owners take their ready sites (barrier), visit them and decrement
-      // the wait counts of the neighbours they precede (fire-and-forget shared
-      // atomics), and the round's sums are reduced (barrier).
+      // ---- rounds: a site is ready once its wait count is 0.  Each round the
+      // owners take their ready sites (barrier), visit them and decrement the
+      // counts of the neighbours they precede, and the round's sums are
+      // reduced (barrier).
       for (int r = 1;; r++) {
         if (r > 4096) {  // no progress: cannot happen on a consistent order
           if (tid == 0) atomicExch(a.err, GSB_EUNSUPPORTED);
@@ -203,10 +234,10 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
         int left = 0;
 #pragma unroll
         for (int j = 0; j < KW; j++) {
-          uint32_t z = 0;  // sites whose 4-bit count is 0
+          uint32_t z = 0;  // offsets whose 4-bit count is 0
 #pragma unroll
           for (int b8 = 0; b8 < 4; b8++) {
-            const uint32_t x = cnt[(v0 >> 3) + 4 * j + b8];
+            const uint32_t x = cnt[(4 * j + b8) * NT + tid];
             uint32_t y = ~(x | (x >> 1) | (x >> 2) | (x >> 3)) & 0x11111111u;
             y = (y | (y >> 3)) & 0x03030303u;  // nibble flags -> 8 bits
             y = (y | (y >> 6)) & 0x000F000Fu;
@@ -227,32 +258,41 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
           while (m) {
             const int b = __ffs(m) - 1;
             m &= m - 1;
-            const int v = v0 + 32 * j + b;
+            const int o = 32 * j + b, v = v0 + o;
             int nb[4];
             nbr(v, nb[0], nb[1], nb[2], nb[3]);
-            const uint32_t e = em[v];
+            const uint32_t mv = meta[o * NT + tid];
+            const uint32_t mu = meta[tix(nb[0])], md = meta[tix(nb[1])];
+            const uint32_t ml = meta[tix(nb[2])], mr = meta[tix(nb[3])];
 #pragma unroll
             for (int d = 0; d < 4; d++)
-              if (!((e >> d) & 1u)) atomicSub(&cnt[nb[d] >> 3], 1u << (4 * (nb[d] & 7)));
-            const int sv = s[v];
-            const int h = __ldg(&a.w[2 * v]) * s[nb[3]] + __ldg(&a.w[2 * v + 1]) * s[nb[1]] +
-                          __ldg(&a.w[2 * nb[2]]) * s[nb[2]] + __ldg(&a.w[2 * nb[0] + 1]) * s[nb[0]];
-            const int delta = sv * h;
+              if (!((mv >> d) & 1u)) {
+                const int u = nb[d], ou = u & (K - 1);
+                atomicSub(&cnt[(ou >> 3) * NT + (u >> LK)], 1u << (4 * (ou & 7)));
+              }
+            // Delta = s_v * sum_j w_vj s_j; a term is -1 iff (w < 0) != (s_j < 0)
+            const uint32_t neg = (((mv >> 4) ^ (mr >> 6) ^ 1u) & 1u) |
+                                 ((((mv >> 5) ^ (md >> 6) ^ 1u) & 1u) << 1) |
+                                 ((((ml >> 4) ^ (ml >> 6) ^ 1u) & 1u) << 2) |
+                                 ((((mu >> 5) ^ (mu >> 6) ^ 1u) & 1u) << 3);
+            const int h = 4 - 2 * __popc(neg);
+            const int delta = (mv & RS_SP) ? h : -h;
             bool acc;
             if (SA) {
               acc = delta >= 0;
-              if (!acc) acc = (uint64_t)pu[v] < (delta == -2 ? Kd2 : delta == -4 ? Kd4 : 0ull);
+              if (!acc) acc = (uint64_t)pu[o * NT + tid] < (delta == -2 ? Kd2 : delta == -4 ? Kd4 : 0ull);
             } else {
               acc = delta > 0;
             }
             if (acc) {
-              s[v] = (int8_t)-sv;
-              dl[v] = (int8_t)delta;
+              meta[o * NT + tid] = (uint8_t)(mv ^ RS_SP);
+              dl[o * NT + tid] = (int8_t)delta;
               fl[j] |= 1u << b;
               D += delta;
               if (delta > 0) P += delta;
             }
           }
+          sb[j] ^= fl[j];
         }
         // ---- round totals (partials double-buffered by parity)
         int all_left;
@@ -285,7 +325,7 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
             while (m) {
               const int b = __ffs(m) - 1;
               m &= m - 1;
-              ws += dl[v0 + 32 * j + b];
+              ws += dl[(32 * j + b) * NT + tid];
             }
           }
           int x = ws;  // inclusive warp scan, then the warps' totals
@@ -305,12 +345,11 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
             while (m) {
               const int b = __ffs(m) - 1;
               m &= m - 1;
-              const int v = v0 + 32 * j + b;
-              const int d = dl[v];
+              const int d = dl[(32 * j + b) * NT + tid];
               run += d;
               if (d > 0) {
                 const long long kk = (long long)(((unsigned long long)(unsigned)run << 32) |
-                                                 (0xFFFFFFFFu - (uint32_t)v));
+                                                 (0xFFFFFFFFu - (uint32_t)(v0 + 32 * j + b)));
                 key = kk > key ? kk : key;
               }
             }
@@ -324,16 +363,12 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
           if (key != LLONG_MIN && mval > best) {
             best = mval;
             const int vstar = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFll));
+            // own spins now, minus this round's flips after the maximum
 #pragma unroll
             for (int j = 0; j < KW; j++) {
-              // current spins, minus this round's flips after the maximum
-              uint32_t b = 0;
-              for (int i = 0; i < 32; i++) {
-                const int v = v0 + 32 * j + i;
-                const bool undo = ((fl[j] >> i) & 1u) && v > vstar;
-                b |= ((s[v] > 0) != undo ? 1u : 0u) << i;
-              }
-              bst[tid * KW + j] = b;
+              const int first = vstar - (v0 + 32 * j);  // offsets > first are after it
+              const uint32_t after = first < 0 ? 0xFFFFFFFFu : first >= 31 ? 0u : (0xFFFFFFFFu << (first + 1));
+              bst[j * NT + tid] = sb[j] ^ (fl[j] & after);
             }
           }
           __syncthreads();  // sh.scan / sh.kred reused by the next round
@@ -347,23 +382,22 @@ __global__ void __launch_bounds__(RS_MAXNT) rscan_kernel(RsArgs a) {
 
     // ---- integrity guard (solvers.py:132-133): recompute the cut of best
     __syncthreads();
-    const int cb = block_sum(own_cut([&](int v) { return (int)((bst[v >> 5] >> (v & 31)) & 1u); }));
+    const int cb = block_sum(own_cut(bst_bit));
     if (tid == 0) {
       a.best_cut[trial] = best;
       a.sweeps_exec[trial] = executed;
       if (cb != best) atomicExch(a.err, GSB_EINTEGRITY);
     }
-    // ---- best spins MSB-first by site id
+    // ---- best spins MSB-first by site id: byte B holds sites 8B..8B+7, all
+    // owned by one thread (K is a multiple of 8)
     uint8_t *out = a.best_bits + (size_t)trial * a.nbytes;
-    for (int byte = tid; byte < a.nbytes; byte += blockDim.x) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const int x = byte * 8 + q;
-        const uint32_t bit = x < n ? (bst[x >> 5] >> (x & 31)) & 1u : 0u;
-        v |= bit << (7 - q);
-      }
-      out[byte] = (uint8_t)v;
+    for (int byte = tid; byte < a.nbytes; byte += NT) {
+      const int v = 8 * byte;
+      const int o = v & (K - 1);
+      const uint32_t w8 = (bst[(o >> 5) * NT + (v >> LK)] >> (o & 31)) & 0xFFu;
+      uint32_t bits = __brev(w8) >> 24;  // site 8B -> MSB
+      if (v + 8 > n) bits &= 0xFFu << (v + 8 - n);  // padding bits 0
+      out[byte] = (uint8_t)bits;
     }
     __syncthreads();
   }
@@ -378,8 +412,8 @@ static int rs_kw(int n) {
   return 0;
 }
 
-static size_t rs_smem(int npad) {  // pu, bst, cnt, s, em, dl
-  return (size_t)npad * 4 + (size_t)npad / 8 + (size_t)npad / 2 + (size_t)npad * 3;
+static size_t rs_smem(int npad) {  // pu, bst, cnt, meta, dl
+  return (size_t)npad * 4 + (size_t)npad / 8 + (size_t)npad / 2 + (size_t)npad * 2;
 }
 
 bool rscan_fits(int rows, int cols) {
