@@ -434,6 +434,24 @@ def main():
                       "workload": f"simulated_annealing (bit-exact numpy-PCG64 + permutation "
                                   f"engine), torus {rows}x{cols}:1, 1024 trials x 1000 sweeps",
                       "ms": rt * 1e3}
+        # the random-scan kind: the reference's dynamics in law (final-cut
+        # distribution agrees with run_trial's; DESIGN.md random-scan contract)
+        from paper_2505_18508_b200.solvers import rscan_fits
+
+        if rscan_fits(rows, cols):
+            scfg = default_config("simulated_annealing_random_scan", 1000, 0)
+            run_trials_device(inst, scfg, rseeds[:32], device=dev)
+            torch.cuda.synchronize()
+            r0.record(stream)
+            run_trials_device(inst, scfg, rseeds, device=dev, check=False)
+            r1.record(stream)
+            torch.cuda.synchronize()
+            st_ = r0.elapsed_time(r1) / 1e3
+            ref_engine["random_scan"] = {
+                "value": 1024 * 1000 * n / st_, "unit": "spin-updates/s",
+                "workload": f"simulated_annealing_random_scan (Philox priorities, level-by-level "
+                            f"random visit order), torus {rows}x{cols}:1, 1024 trials x 1000 sweeps",
+                "ms": st_ * 1e3}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:

@@ -116,6 +116,10 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
                     int64_t *best_cut_dev, int32_t *sweeps_executed_dev, uint8_t *best_bits_dev,
                     void *workspace_dev, size_t workspace_bytes, void *stream);
 
+/* 1 if a rows x cols torus fits the random-scan engine (GSB_ENGINE_RANDOM_SCAN:
+ * one trial's state in one SM's shared memory, cols <= 16384), else 0. */
+int gsb_rscan_fits(int32_t rows, int32_t cols);
+
 /* The sweep calls are asynchronous on `stream`.  The integrity guard of
  * solvers.py:132-133 (best_cut == cut of the best bitstring, recomputed on
  * the device) is recorded in the workspace; gsb_workspace_status synchronises

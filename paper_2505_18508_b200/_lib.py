@@ -81,6 +81,7 @@ def lib():
         L.gsb_torus_sweep_host.argtypes = [i32, i32, P, ctypes.c_int, ctypes.c_int, i32, dbl, dbl,
                                            P, i32, P, P, P, P]
         L.gsb_workspace_status.argtypes = [P, P]
+        L.gsb_rscan_fits.argtypes = [i32, i32]
         L.gsb_workspace_counters.argtypes = [P, P, P]
         L.gsb_philox_bench.argtypes = [i64, P, P]
         L.gsb_best_key.argtypes = [P, i32, i64, P, P]

@@ -235,6 +235,8 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   return rc;
 }
 
+int gsb_rscan_fits(int32_t rows, int32_t cols) { return rscan_fits(rows, cols) ? 1 : 0; }
+
 int gsb_workspace_counters(const void *ws, void *stream, uint64_t *philox_blocks) {
   if (!ws || !philox_blocks) return set_error(GSB_EINVAL, "null argument");
   cudaStream_t st = (cudaStream_t)stream;

@@ -167,6 +167,11 @@ def _graph_dmax(instance: ProblemInstance) -> int:
     return max(int(tot.max()) if tot.size else 1, 1)
 
 
+def rscan_fits(rows: int, cols: int) -> bool:
+    """Whether a rows x cols torus fits the random-scan engine (one SM's shared memory)."""
+    return _lib.lib().gsb_rscan_fits(rows, cols) == 1
+
+
 def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, device=None,
                       stream=None, check: bool = True, engine: int | None = None):
     """Batched trials with device-resident outputs (torch tensors).
