@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -220,6 +221,11 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     } else {
       return set_error(GSB_EUNSUPPORTED, "torus too large for the checkerboard engines");
     }
+  } else if (engine == GSB_ENGINE_RANDOM_SCAN && !getenv("GSB_RSCAN_SCALAR") &&
+             rscan_bs_fits(inst->rows, inst->cols)) {
+    // bit-sliced rounds; the per-site kernel (same results) is the fallback
+    rc = rscan_bs_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
+                      sweeps_exec, best_bits, err, stream);
   } else if (engine == GSB_ENGINE_RANDOM_SCAN) {
     rc = rscan_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
                    sweeps_exec, best_bits, err, stream);
@@ -235,7 +241,9 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   return rc;
 }
 
-int gsb_rscan_fits(int32_t rows, int32_t cols) { return rscan_fits(rows, cols) ? 1 : 0; }
+int gsb_rscan_fits(int32_t rows, int32_t cols) {
+  return rscan_bs_fits(rows, cols) || rscan_fits(rows, cols) ? 1 : 0;
+}
 
 int gsb_workspace_counters(const void *ws, void *stream, uint64_t *philox_blocks) {
   if (!ws || !philox_blocks) return set_error(GSB_EINVAL, "null argument");
