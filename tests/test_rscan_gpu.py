@@ -122,3 +122,18 @@ def test_checkerboard_order_shifts_the_distribution():
     c = _final_cuts(inst, ANNEALING_CHECKERBOARD, 1000, 1024)
     se = np.sqrt(a.var(ddof=1) / len(a) + c.var(ddof=1) / len(c))
     assert c.mean() - a.mean() > 4 * se
+
+
+@pytest.mark.parametrize("R,C", [(3, 5), (10, 33), (50, 100), (100, 100), (64, 200)])
+def test_random_scan_kernels_agree(R, C, monkeypatch):
+    """The bit-sliced kernel (default) and the per-site kernel (fallback,
+    GSB_RSCAN_SCALAR=1) run the same contract: identical results."""
+    inst = generate_torus(TorusSpec(R, C, 4))
+    seeds = mix_seeds(MASTER, range(40))
+    for cfg in (default_config(ANNEALING_RANDOM_SCAN, 25, 0), default_config(GREEDY_RANDOM_SCAN, 50, 0)):
+        a = run_trials(inst, cfg, seeds)
+        monkeypatch.setenv("GSB_RSCAN_SCALAR", "1")
+        b = run_trials(inst, cfg, seeds)
+        monkeypatch.delenv("GSB_RSCAN_SCALAR")
+        assert np.array_equal(a.best_cut, b.best_cut) and np.array_equal(a.bits, b.bits)
+        assert np.array_equal(a.sweeps_executed, b.sweeps_executed)
