@@ -254,7 +254,7 @@ def main():
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
-    launches_per_step = 3  # checker masks + sweep kernel + best-key kernel (ours)
+    launches_per_step = 4  # checker masks + geo2 tables + sweep kernel + best-key kernel (ours)
 
     def sweep_launch():
         _lib.check(L.gsb_torus_sweep(ts, cfg.engine, kind_code, S,
