@@ -30,6 +30,7 @@
 // reaching a new maximum above `best` defines the snapshot.
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "gsb_device.cuh"
 #include "gsb_internal.h"
@@ -60,6 +61,12 @@ __device__ __forceinline__ u128 shfl128(u128 v, int src) {
 
 __device__ __forceinline__ int getbit(const uint32_t *a, int x) { return (a[x >> 5] >> (x & 31)) & 1; }
 
+// V2 (default): Fisher-Yates batches of up to 64 draws (all 32 computed
+// outputs used; draws lane and lane + 32 per lane, duplicate targets found
+// with the `mark` bitmap) and the visit batches' best-so-far scan gated on
+// cur + (sum of positive committed Deltas) > best.  V1: 32-draw batches,
+// ungated scan (kept for A/B, GSB_REFWARP_V1=1).
+template <bool V2>
 __global__ void __launch_bounds__(32) ref_warp_kernel(RefWarpArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = a.n, nwd = a.nwords, lane = threadIdx.x;
@@ -146,11 +153,101 @@ __global__ void __launch_bounds__(32) ref_warp_kernel(RefWarpArgs a) {
         mask |= mask >> 8;
         mask |= mask >> 16;
         const int half = (int)((mask + 1) >> 1);
-        const int nb = min(32, i - half + 1);  // mask constant for lanes < nb
-        // draw lane: next32 #lane of the stream
         const int h = has32;
         const u128 sl = Aj * s + Cj;
         const uint64_t o = pcg_out(sl);
+        if (V2) {
+          // draws k = lane (set A) and k = lane + 32 (set B); draw k is the
+          // buffered half if k < h, else half (k-h)&1 of output (k-h)>>1
+          const int nb = min(64, i - half + 1);  // mask constant for draws < nb
+          const uint32_t olo = (uint32_t)o, ohi = (uint32_t)(o >> 32);
+          const int qa = lane - h, qb = lane + 32 - h;
+          const int sa = qa >= 0 ? (qa >> 1) : 0, sb = qb >> 1;
+          const uint32_t alo = __shfl_sync(FULL, olo, sa), ahi = __shfl_sync(FULL, ohi, sa);
+          const uint32_t blo = __shfl_sync(FULL, olo, sb), bhi = __shfl_sync(FULL, ohi, sb);
+          const int va = (int)((qa < 0 ? buf : ((qa & 1) ? ahi : alo)) & mask);
+          const int vb = (int)(((qb & 1) ? bhi : blo) & mask);
+          const int kb = lane + 32;
+          const bool ina = lane < nb, inb = kb < nb;
+          // draw k is accepted for sure if v <= i - k, rejected if v > i
+          const bool sacc_a = ina && va <= i - lane, sacc_b = inb && vb <= i - kb;
+          const unsigned ambA = __ballot_sync(FULL, ina && !sacc_a && va <= i);
+          const unsigned ambB = __ballot_sync(FULL, inb && !sacc_b && vb <= i);
+          int L = ambA ? __ffs(ambA) - 1 : ambB ? 31 + __ffs(ambB) : nb;  // draw 0 is never ambiguous
+          unsigned mA = __ballot_sync(FULL, sacc_a), mB = __ballot_sync(FULL, sacc_b);
+          mA &= L >= 32 ? FULL : (1u << L) - 1u;
+          mB &= L >= 64 ? FULL : L <= 32 ? 0u : (1u << (L - 32)) - 1u;
+          const int na = __popc(mA), nacc = na + __popc(mB);
+          const bool ea = (mA >> lane) & 1u, eb = (mB >> lane) & 1u;
+          const int ila = i - __popc(mA & lt_mask), ilb = i - na - __popc(mB & lt_mask);
+          // a target inside the batch's position window is the position of
+          // the (later) accepted draw of rank i - v
+          int cfirst = 64;
+          auto window = [&](bool e, int v, int il) {
+            if (e && v != il && v > i - nacc) {
+              const int r2 = i - v;
+              const int k2 = r2 < na ? (int)__fns(mA, 0, r2 + 1) : 32 + (int)__fns(mB, 0, r2 - na + 1);
+              cfirst = min(cfirst, k2);
+            }
+          };
+          window(ea, va, ila);
+          window(eb, vb, ilb);
+          // duplicate targets: the draw that finds its bit already set conflicts
+          // (set A before set B; within a set the order is arbitrary, which can
+          // only cut earlier than needed)
+          if (ea && (atomicOr(&mark[va >> 5], 1u << (va & 31)) >> (va & 31)) & 1u)
+            cfirst = min(cfirst, lane);
+          __syncwarp();
+          if (eb && (atomicOr(&mark[vb >> 5], 1u << (vb & 31)) >> (vb & 31)) & 1u)
+            cfirst = min(cfirst, kb);
+          __syncwarp();
+          if (ea) mark[va >> 5] = 0u;  // only this batch's bits are set
+          if (eb) mark[vb >> 5] = 0u;
+          cfirst = (int)__reduce_min_sync(FULL, (unsigned)cfirst);
+          if (cfirst < L) {
+            L = max(cfirst, 1);  // draw 0 alone is always exact
+            mA &= L >= 32 ? FULL : (1u << L) - 1u;
+            mB &= L <= 32 ? 0u : (1u << (L - 32)) - 1u;
+          }
+          // execute the committed swaps (disjoint positions)
+          const bool doa = (mA >> lane) & 1u, dob = (mB >> lane) & 1u;
+          uint16_t pa0 = 0, pa1 = 0, pb0 = 0, pb1 = 0;
+          if (doa) {
+            pa0 = perm[ila];
+            pa1 = perm[va];
+          }
+          if (dob) {
+            pb0 = perm[ilb];
+            pb1 = perm[vb];
+          }
+          __syncwarp();
+          if (doa) {
+            perm[ila] = pa1;
+            perm[va] = pa0;
+          }
+          if (dob) {
+            perm[ilb] = pb1;
+            perm[vb] = pb0;
+          }
+          __syncwarp();
+          i -= __popc(mA) + __popc(mB);
+          const int fresh = L - h;
+          if (fresh <= 0) {
+            has32 = 0;
+          } else {
+            const int outs = (fresh + 1) >> 1;
+            s = shfl128(sl, outs - 1);
+            if (fresh & 1) {
+              has32 = 1;
+              buf = __shfl_sync(FULL, ohi, outs - 1);
+            } else {
+              has32 = 0;
+            }
+          }
+          continue;
+        }
+        const int nb = min(32, i - half + 1);  // mask constant for lanes < nb
+        // draw lane: next32 #lane of the stream
         const int q = lane - h;  // index among fresh halves
         const int src = q >= 0 ? (q >> 1) : 0;
         const uint64_t ov = __shfl_sync(FULL, (unsigned long long)o, src);
@@ -269,8 +366,25 @@ __global__ void __launch_bounds__(32) ref_warp_kernel(RefWarpArgs a) {
         const int L = hitm ? max(__ffs(hitm) - 1, 1) : nb;
         const bool commit = acc && lane < L;
         const unsigned cm = __ballot_sync(FULL, commit);
-        // running cut and the first new maximum (strict >, solvers.py:125)
+        // running cut and the first new maximum (strict >, solvers.py:125);
+        // V2 scans only if the positive committed Deltas can lift cur above best
         int pre = commit ? delta : 0;
+        if (V2) {
+          const int tot = (int)__reduce_add_sync(FULL, (unsigned)pre);
+          const int pos = (int)__reduce_add_sync(FULL, (unsigned)(pre > 0 ? pre : 0));
+          if (cur + pos <= best) {
+            if (commit) atomicXor(&spins[x >> 5], 1u << (x & 31));
+            cur += tot;
+            if (cm) flipped = true;
+            if (a.sa) {
+              const int used = __popc(negm & ((L >= 32) ? FULL : ((1u << L) - 1u)));
+              if (used) s = shfl128(sl, used - 1);
+            }
+            __syncwarp();
+            k0 += L;
+            continue;
+          }
+        }
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const int y = __shfl_up_sync(FULL, pre, off);
@@ -385,18 +499,19 @@ int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.inv_cols = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)cols - 1) / (uint64_t)cols);
   a.err = err_ws;
   const size_t smem = ref_warp_smem(n);
+  auto kern = getenv("GSB_REFWARP_V1") ? ref_warp_kernel<false> : ref_warp_kernel<true>;
   if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(ref_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem) != cudaSuccess)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
     return set_error(GSB_ECUDA, "cudaFuncSetAttribute failed");
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ref_warp_kernel, 32, smem) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) !=
           cudaSuccess ||
       per_sm < 1)
     return set_error(GSB_ECUDA, "reference warp kernel does not fit");
   int grid = nsm * per_sm;
   if (grid > T) grid = T;
-  ref_warp_kernel<<<grid, 32, smem, stream>>>(a);
+  kern<<<grid, 32, smem, stream>>>(a);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
 }
