@@ -157,7 +157,12 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
   const uint4 *__restrict__ msk = a.masks;        // [2][nw]
   const uint4 *__restrict__ geo = a.geo;          // [nw]
   const uint4 *__restrict__ geo2 = a.geo2;        // [2][nw][2]
-  uint32_t *st = (uint32_t *)smem_raw;            // [2][nw] neighbour copy
+  // per-trial Philox precomputation of the plane blocks (philox10_from2):
+  // tabP[p][wi] = M0*x2 of (wi, q = 2p) and (wi, q = 2p + 1), tabW[wi] = (c1, c2);
+  // each thread reads only the entries of its own words
+  uint4 *tabP = (uint4 *)smem_raw;                // [2][nw]
+  uint2 *tabW = (uint2 *)(tabP + 2 * nw);         // [nw]
+  uint32_t *st = (uint32_t *)(tabW + nw);         // [2][nw] neighbour copy
   uint32_t *bst = st + 2 * nw;                    // [2][nw] best snapshot
   uint32_t *tx = bst + 2 * nw;                    // [NWARP][3][WPT][32] tail exchange
   uint32_t *tq = tx + NWARP * 3 * WPT * 32;       // [NWARP][32] tail queue
@@ -203,6 +208,17 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
           if (p == 0) cur_w[j] = s0; else oth_w[j] = s0;
           st[p * nw + wi] = s0;
           bst[p * nw + wi] = s0;
+        }
+        if (SA) {
+          uint32_t h1z, a0, b0, a1, b1;
+          const PhiloxWord pw = philox_word((uint32_t)wi, key0, key1, h1z);
+          tabW[wi] = make_uint2(pw.c1, pw.c2);
+#pragma unroll
+          for (int p = 0; p < 2; p++) {
+            philox_pre(h1z, 2u * p, key0, a0, b0);
+            philox_pre(h1z, 2u * p + 1u, key0, a1, b1);
+            tabP[p * nw + wi] = make_uint4(a0, b0, a1, b1);
+          }
         }
       }
     }
@@ -256,6 +272,12 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
       for (int p = 0; p < 2; p++, buf ^= 1) {
         uint32_t A[WPT], c2[WPT], eq[WPT], lt[WPT];
         int wpos[WPT], wsum[WPT];
+        // rounds 0-1 of the plane blocks that depend only on (t, q): uniform
+        uint32_t u1a = 0, va = 0, u1b = 0, vb = 0;
+        if (SA) {
+          philox_uni((uint32_t)t, 2u * p, key0, key1, u1a, va);
+          philox_uni((uint32_t)t, 2u * p + 1u, key0, key1, u1b, vb);
+        }
         // ---- pass 1: classes and the unconditional planes 0-7.  Words j <
         // WPT-1 are owned by every lane (the launch picks WPT = ceil(nw/NT)),
         // so only the last one is guarded and the bodies schedule together.
@@ -280,10 +302,12 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
                 wsum[j] = wpos[j];  // minus the accepted Delta<0 flips at commit
                 const uint32_t e2 = c.km2 & me2, e4 = c.km4 & me4;
                 c2[j] = e2;
-                const P4 r0 =
-                    philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p), 1u}, key0, key1);
-                const P4 r1 =
-                    philox10(P4{(uint32_t)wi, (uint32_t)t, (uint32_t)(2 * p + 1), 1u}, key0, key1);
+                // Philox(key, (wi, t, 2p + j, 1)), j = 0, 1, from round 2 on
+                const uint4 pre = tabP[p * nw + wi];
+                const uint2 pwv = tabW[wi];
+                const PhiloxWord pw{pwv.x, pwv.y};
+                const P4 r0 = philox10_from2(pw, pre.x, pre.y, u1a, va, key0, key1);
+                const P4 r1 = philox10_from2(pw, pre.z, pre.w, u1b, vb, key0, key1);
                 cmp_planes<L>(r0, r1, e2, e2 | e4, K2, K4, eq[j], lt[j]);
               } else {
                 A[j] = c.k3 | c.k4;
@@ -596,7 +620,8 @@ __global__ void __launch_bounds__(NT, MINB) checker_sweep_kernel(CheckerArgs a) 
 // ------------------------------------------------------------------ launch
 static size_t smem_bytes(int nw, int NT, int WPT) {
   const int NWARP = NT / 32;
-  size_t b = (size_t)4 * nw * 4;                            // st, bst
+  size_t b = (size_t)2 * nw * 16 + (size_t)nw * 8;          // tabP, tabW
+  b += (size_t)4 * nw * 4;                                  // st, bst
   b += (size_t)NWARP * 3 * WPT * 32 * 4 + (size_t)NWARP * 32 * 4;  // tail exchange + queue
   b += (size_t)(6 * NWARP) * 4;
   b += (size_t)((WPT * NWARP + 1) & ~1) * 4;
