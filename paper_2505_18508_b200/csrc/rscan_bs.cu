@@ -202,36 +202,42 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
         const bool valid = c < cols;
         const int cc = valid ? c : 0;
         const int v = r * cols + cc;
-        const int vu = (r == 0 ? rows - 1 : r - 1) * cols + cc;
         const int vd = (r == rows - 1 ? 0 : r + 1) * cols + cc;
-        const int vl = r * cols + (cc == 0 ? cols - 1 : cc - 1);
         const int vr = r * cols + (cc == cols - 1 ? 0 : cc + 1);
         const uint32_t pv = prio[v];
         auto prec = [&](int u) {
           const uint32_t pn = prio[u];
           return (int)valid & ((int)(pn < pv) | ((int)(pn == pv) & (int)(u < v)));
         };
-        const uint32_t eu = __ballot_sync(0xffffffffu, prec(vu));
+        // only the down and right planes: "precedes" is a strict total order,
+        // so up(v) = !down(v - cols) and left(v) = !right(v - 1) (below)
         const uint32_t ed = __ballot_sync(0xffffffffu, prec(vd));
-        const uint32_t el = __ballot_sync(0xffffffffu, prec(vl));
         const uint32_t er = __ballot_sync(0xffffffffu, prec(vr));
         uint32_t pl[8];
         const uint32_t byte = valid ? ub[v] : 0u;
 #pragma unroll
         for (int jj = 0; jj < 8; jj++) pl[jj] = __ballot_sync(0xffffffffu, (byte >> (7 - jj)) & 1u);
         if (lane == 0) {
-          E[w] = eu;
           E[nw + w] = ed;
-          E[2 * nw + w] = el;
           E[3 * nw + w] = er;
           U[w] = vmask(k);
-        }
-        if (SA && lane < 8) {
-          uint32_t x = pl[0];
+          if (SA) {
 #pragma unroll
-          for (int jj = 1; jj < 8; jj++) x = lane == jj ? pl[jj] : x;
-          PL[lane * nw + w] = x;
+            for (int jj = 0; jj < 8; jj++) PL[jj * nw + w] = pl[jj];
+          }
         }
+      }
+      __syncthreads();
+      // up and left planes of the own words from the down / right planes of
+      // the neighbours (padding bits stay 0)
+#pragma unroll
+      for (int j = 0; j < WPT; j++) {
+        if (!own[j]) continue;
+        const int w = j * RB_NT + tid;
+        const int r = orow[j], k = ocol[j];
+        const uint32_t V = vmask(k);
+        E[w] = ~E[nw + upw(r, k)] & V;
+        E[2 * nw + w] = ~alignL(E + 3 * nw, w, r, k) & V;
       }
       __syncthreads();
       bool sweep_flipped = false;
