@@ -8,8 +8,9 @@
 //   1. priorities and uniforms, one Philox block per 4 consecutive sites
 //      (lane per quad): priorities to shared memory, uniform top bytes too;
 //   2. lane per site, warp per word: the preceding-neighbour planes E[4][w]
-//      (ballots of the four comparisons) and the uniform's top 8 bits as
-//      planes PL[8][w] (ballots);
+//      (ballots of the down and right comparisons; up and left follow from
+//      them because "precedes" is a strict total order) and the uniform's top 8 bits as
+//      planes PL4[w][2] (ballots; 8 planes per word, 32 B);
 //   3. rounds, lane per word: ready = unvisited sites whose preceding
 //      neighbours are all visited (bit-sliced over the unvisited planes of the
 //      four aligned neighbour words), Delta classes, the 8-plane comparison
@@ -57,11 +58,11 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
   const int rows = a.rows, cols = a.cols, n = a.n, WPR = a.WPR, nw = a.nw, lb = a.lb;
   const int nq = (n + 3) >> 2;
   uint32_t *prio = (uint32_t *)smem_raw;  // [4 * nq] per site
-  uint32_t *S = prio + 4 * nq;            // [nw] spins (1 = +1)
+  uint4 *PL4 = (uint4 *)(prio + 4 * nq);  // [nw][2] uniform bits 31..24 (planes 0-3, 4-7)
+  uint32_t *S = (uint32_t *)(PL4 + 2 * nw);  // [nw] spins (1 = +1)
   uint32_t *U = S + nw;                   // [nw] unvisited this sweep
   uint32_t *E = U + nw;                   // [4][nw] preceding neighbour: up, down, left, right
-  uint32_t *PL = E + 4 * nw;              // [8][nw] uniform bit 31 - j
-  uint32_t *NC = PL + 8 * nw;             // [4][nw] coupling < 0: right, left, up, down neighbour
+  uint32_t *NC = E + 4 * nw;              // [4][nw] coupling < 0: right, left, up, down neighbour
   uint32_t *BS = NC + 4 * nw;             // [nw] best snapshot
   uint8_t *ub = (uint8_t *)(BS + nw);     // [4 * nq] uniform top bytes
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -191,10 +192,12 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
       // ---- 2. preceding-neighbour and uniform planes (warp per word)
       int r2, k2;
       wgeo(warp, r2, k2);
+      const int dr = RB_NWARP / WPR, dk = RB_NWARP - dr * WPR;  // word step in (row, column word)
       for (int w = warp; w < nw; w += RB_NWARP) {
         const int r = r2, k = k2;
-        k2 += RB_NWARP;
-        while (k2 >= WPR) {
+        k2 += dk;
+        r2 += dr;
+        if (k2 >= WPR) {
           k2 -= WPR;
           r2++;
         }
@@ -222,8 +225,8 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
           E[3 * nw + w] = er;
           U[w] = vmask(k);
           if (SA) {
-#pragma unroll
-            for (int jj = 0; jj < 8; jj++) PL[jj * nw + w] = pl[jj];
+            PL4[2 * w] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+            PL4[2 * w + 1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
           }
         }
       }
@@ -283,8 +286,9 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
           if (SA) {
             const uint32_t e2 = c.km2 & me2 & ready, e4 = c.km4 & me4 & ready;
             uint32_t eq, lt;
-            const P4 r0{PL[w], PL[nw + w], PL[2 * nw + w], PL[3 * nw + w]};
-            const P4 r1{PL[4 * nw + w], PL[5 * nw + w], PL[6 * nw + w], PL[7 * nw + w]};
+            const uint4 pa = PL4[2 * w], pb = PL4[2 * w + 1];
+            const P4 r0{pa.x, pa.y, pa.z, pa.w};
+            const P4 r1{pb.x, pb.y, pb.z, pb.w};
             cmp_planes<0>(r0, r1, e2, e2 | e4, K2, K4, eq, lt);
             // undecided sites (top byte equal to K's): the low 24 bits
             while (eq) {
