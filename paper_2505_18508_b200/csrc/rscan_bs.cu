@@ -51,6 +51,17 @@ struct RbShared {
   long long kred[RB_NWARP];
 };
 
+// ballot of (x & m) != 0: one LOP3 with a predicate result and one VOTE (the
+// C++ form compiles to shift, and, compare and predicate spills)
+__device__ __forceinline__ uint32_t ballot_bit(uint32_t x, uint32_t m) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\t"
+      "setp.ne.u32 p, t, 0;\n\tvote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+      : "=r"(r)
+      : "r"(x), "r"(m));
+  return r;
+}
+
 template <int WPT, bool SA>
 __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
         uint32_t pl[8];
         const uint32_t byte = valid ? ub[v] : 0u;
 #pragma unroll
-        for (int jj = 0; jj < 8; jj++) pl[jj] = __ballot_sync(0xffffffffu, (byte >> (7 - jj)) & 1u);
+        for (int jj = 0; jj < 8; jj++) pl[jj] = ballot_bit(byte, 0x80u >> jj);
         if (lane == 0) {
           E[nw + w] = ed;
           E[3 * nw + w] = er;
