@@ -17,7 +17,7 @@
 //      with the sweep's thresholds (undecided sites draw their block again and
 //      compare the low 24 bits), commit, Delta sums, and best-so-far in
 //      (round, id) order exactly as the checkerboard engine does per
-//      half-sweep.  Two barriers per round (ready sets before any commit).
+//      half-sweep.  One barrier per round (the round totals; see below).
 #include <climits>
 #include <cstdint>
 
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
   uint32_t *prio = (uint32_t *)smem_raw;  // [4 * nq] per site
   uint4 *PL4 = (uint4 *)(prio + 4 * nq);  // [nw][2] uniform bits 31..24 (planes 0-3, 4-7)
   uint32_t *S = (uint32_t *)(PL4 + 2 * nw);  // [nw] spins (1 = +1)
-  uint32_t *U = S + nw;                   // [nw] unvisited this sweep
-  uint32_t *E = U + nw;                   // [4][nw] preceding neighbour: up, down, left, right
+  uint32_t *U = S + nw;                   // [2][nw] unvisited, by round parity
+  uint32_t *E = U + 2 * nw;               // [4][nw] preceding neighbour: up, down, left, right
   uint32_t *NC = E + 4 * nw;              // [4][nw] coupling < 0: right, left, up, down neighbour
   uint32_t *BS = NC + 4 * nw;             // [nw] best snapshot
   uint8_t *ub = (uint8_t *)(BS + nw);     // [4 * nq] uniform top bytes
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
         if (lane == 0) {
           E[nw + w] = ed;
           E[3 * nw + w] = er;
-          U[w] = vmask(k);
+          U[nw + w] = vmask(k);  // read by round 1
           if (SA) {
             PL4[2 * w] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
             PL4[2 * w + 1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
@@ -263,21 +263,30 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
         }
         uint32_t rd[WPT];
         int left = 0;
+        const uint32_t *Uc = U + (rr & 1) * nw;
+        uint32_t *Un = U + ((rr + 1) & 1) * nw;
 #pragma unroll
         for (int j = 0; j < WPT; j++) {
           rd[j] = 0;
           if (!own[j]) continue;
           const int w = j * RB_NT + tid;
           const int r = orow[j], k = ocol[j];
-          const uint32_t u = U[w];
-          if (!u) continue;
-          const uint32_t block = (E[w] & U[upw(r, k)]) | (E[nw + w] & U[dnw(r, k)]) |
-                                 (E[2 * nw + w] & alignL(U, w, r, k)) |
-                                 (E[3 * nw + w] & alignR(U, w, r, k));
+          const uint32_t u = Uc[w];
+          if (!u) {
+            Un[w] = 0u;
+            continue;
+          }
+          const uint32_t block = (E[w] & Uc[upw(r, k)]) | (E[nw + w] & Uc[dnw(r, k)]) |
+                                 (E[2 * nw + w] & alignL(Uc, w, r, k)) |
+                                 (E[3 * nw + w] & alignR(Uc, w, r, k));
           rd[j] = u & ~block;
-          left += __popc(u & ~rd[j]);
+          Un[w] = u & block;
+          left += __popc(u & block);
         }
-        __syncthreads();  // ready sets fixed before any commit
+        // No barrier before the commits: two sites ready in the same round are
+        // never neighbours (one precedes the other), so every bit a ready
+        // site's Delta reads is stable during the round, and the unvisited
+        // planes are double-buffered (this round reads Uc, writes Un).
         uint32_t A[WPT];
         int wsum[WPT], wpos[WPT];
         int D = 0, P = 0;
@@ -322,7 +331,6 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
           D += wsum[j];
           P += wpos[j];
           S[w] = s ^ acc;
-          U[w] &= ~ready;
         }
         // ---- round totals
         int all_left;
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
 // ------------------------------------------------------------------ host
 static size_t rb_smem(int n, int nw) {
   const size_t nq = (size_t)(n + 3) / 4;
-  return nq * 16 + (size_t)nw * 4 * 19 + nq * 4;
+  return nq * 16 + (size_t)nw * 4 * 20 + nq * 4;
 }
 
 static int rb_wpt(int rows, int cols) {
