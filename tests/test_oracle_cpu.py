@@ -52,6 +52,43 @@ def test_philox_against_torch_and_random123(oracle):
                                                        0x24126EA1]
 
 
+def test_philox_round_split_equals_philox(oracle):
+    """The plane-block decomposition the sweep kernel uses
+    (csrc/gsb_device.cuh: philox_word / philox_pre / philox_uni / philox10_from2)
+    restated in Python: rounds 0-2 of a counter (wi, t, q, 1) split into a
+    per-(wi, q) part and a per-(t, q) part give Philox4x32-10 exactly."""
+    M0, M1, W0, W1, MASK = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85, 0xFFFFFFFF
+
+    def mul(a, b):
+        p = a * b
+        return p >> 32, p & MASK
+
+    def split(wi, t, q, k0, k1):
+        h0, l0 = mul(M0, wi)
+        z1 = h0 ^ 1 ^ k1
+        h1z, l1z = mul(M1, z1)
+        c1, c2 = l0 ^ ((k1 + W1) & MASK), l1z ^ ((k0 + 2 * W0) & MASK)  # per (trial, wi)
+        pre_hi, pre_lo = mul(M0, h1z ^ ((M1 * q) & MASK) ^ ((k0 + W0) & MASK))  # per (trial, wi, q)
+        u1, lo = mul(M0, (M1 * q >> 32) ^ t ^ k0)  # per (trial, t, q)
+        v = lo ^ ((k1 + 2 * W1) & MASK)
+        z2 = u1 ^ c1
+        hi, lo = mul(M1, z2)
+        x, y, z, w = hi ^ c2, lo, pre_hi ^ v, pre_lo
+        for r in range(3, 10):
+            kk0, kk1 = (k0 + r * W0) & MASK, (k1 + r * W1) & MASK
+            h0, l0 = mul(M0, x)
+            h1, l1 = mul(M1, z)
+            x, y, z, w = h1 ^ y ^ kk0, l1, h0 ^ w ^ kk1, l0
+        return [x, y, z, w]
+
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        wi, t = int(rng.integers(0, 1 << 16)), int(rng.integers(0, 1 << 20))
+        q = int(rng.integers(0, 4))
+        k0, k1 = (int(x) for x in rng.integers(0, 1 << 32, size=2, dtype=np.uint64))
+        assert split(wi, t, q, k0, k1) == oracle.philox([wi, t, q, 1], [k0, k1])
+
+
 def test_torus_weights_and_evaluator(oracle):
     for rec in golden("tori.json")["tori"]:
         w = oracle.torus_weights(rec["rows"], rec["cols"], rec["seed"])
