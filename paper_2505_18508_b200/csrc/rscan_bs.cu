@@ -216,8 +216,8 @@ __global__ void __launch_bounds__(RB_NT) rscan_bs_kernel(RbArgs a) {
         const bool valid = c < cols;
         const int cc = valid ? c : 0;
         const int v = r * cols + cc;
-        const int vd = (r == rows - 1 ? 0 : r + 1) * cols + cc;
-        const int vr = r * cols + (cc == cols - 1 ? 0 : cc + 1);
+        const int vd = v + (r == rows - 1 ? cols - n : cols);
+        const int vr = v + (cc == cols - 1 ? 1 - cols : 1);
         const uint32_t pv = prio[v];
         auto prec = [&](int u) {
           const uint32_t pn = prio[u];
