@@ -55,10 +55,10 @@ extern "C" {
 #define GSB_ENGINE_CHECKERBOARD_CLUSTER 3 /* same contract, forces the cluster engine (one trial
                                              over the shared memory of a CTA cluster; used
                                              automatically when the torus exceeds one SM) */
-#define GSB_ENGINE_RANDOM_SCAN 4  /* Philox4x32-10 + the reference's random visit order, drawn
-                                     as priorities and run level by level (DESIGN.md random-scan
-                                     contract): the reference's dynamics in law; any torus
-                                     that fits one SM */
+#define GSB_ENGINE_RANDOM_SCAN 4  /* Philox4x32-10 + the reference's random visit order
+                                     (i.i.d. 32-bit priorities, DESIGN.md random-scan contract):
+                                     solvers.py:107-127 with the same law, best-so-far of the
+                                     sequential scan exact; tori up to 4 warps x 13 rows per lane */
 
 typedef struct gsb_torus {
     int32_t rows, cols;  /* TorusSpec.rows/cols (instances.py:186-187), >= 3 */
@@ -117,8 +117,19 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
                     void *workspace_dev, size_t workspace_bytes, void *stream);
 
 /* 1 if a rows x cols torus fits the random-scan engine (GSB_ENGINE_RANDOM_SCAN:
- * one trial's state in one SM's shared memory, cols <= 16384), else 0. */
+ * cols <= 1024 and rows <= 4 * floor(32 / ceil(cols / 32)) * 13), else 0. */
 int gsb_rscan_fits(int32_t rows, int32_t cols);
+
+/* Team shape the random-scan engine launches for T trials of a rows x cols
+ * torus (one CTA of *warps warps per trial, *rows_per_lane rows per lane);
+ * needs a device (SM count).  Introspection for tests and profiles. */
+int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32_t *rows_per_lane);
+
+/* Counters of the last random-scan sweep call on this workspace: out4[0] =
+ * rounds (summed over trials), [1] sweeps whose best-so-far needed the bucket
+ * pass, [2] candidate buckets sorted exactly, [3] top-byte ties resolved by
+ * low bits.  Synchronises `stream`. */
+int gsb_workspace_rscan_stats(const void *workspace_dev, void *stream, uint64_t *out4);
 
 /* The sweep calls are asynchronous on `stream`.  The integrity guard of
  * solvers.py:132-133 (best_cut == cut of the best bitstring, recomputed on

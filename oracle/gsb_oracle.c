@@ -496,20 +496,28 @@ static int trial_checker(int32_t rows, int32_t cols, const int8_t *w, const int3
 }
 
 /* ------------------------------------------------------------------ */
-/* random-scan (Philox) trial -- DESIGN.md "Random-scan contract"       */
+/* random-scan (Philox) trial -- DESIGN.md "Random-scan contract" (v2)  */
 /* ------------------------------------------------------------------ */
 /* The reference's sweep visits the sites in a fresh uniformly random order
- * (solvers.py:110).  Here the order of sweep t is that of the priorities
- *   p(v) = word (v & 3) of Philox(key, (v >> 2, t, 0, 4)), ties by v,
- * executed level by level: lvl(v) = 1 + max lvl(u) over the neighbours u that
- * precede v (0 if none), visit order (lvl, v).  Every order with each site
- * after its preceding neighbours gives the same spins after each site's visit,
- * so the states at level boundaries and at the end of the sweep are those of
- * the sequential scan in priority order: the reference's dynamics in law, with
- * Philox instead of PCG64.  Other draws:
- *   initial spin of v: top bit of word (v & 3) of Philox(key, (v >> 2, 0, 0, 3));
- *   uniform of v at sweep t: word (v & 3) of Philox(key, (v >> 2, t, 1, 4)),
- *   accept Delta < 0 iff u * 2^-32 < exp(Delta / T_t). */
+ * (solvers.py:110) and, for each, computes Delta, accepts and flips
+ * (solvers.py:111-127).  This restatement keeps solvers.py:107-127 line by
+ * line and changes only where the randomness comes from: the permutation of
+ * sweep t is the sites sorted by (priority, id), the priorities i.i.d. 32-bit
+ * Philox values, and the acceptance uniform of a site is its own 32-bit
+ * Philox value.  Layout of the draws (key = (lo32(seed), hi32(seed)),
+ * TAG = 5, WPR = ceil(cols / 32), site (r, c): word wi = r*WPR + (c >> 5),
+ * bit b = c & 31, id = r*cols + c):
+ *   initial spin:  bit b of word 0 of Philox(key, (wi, 0, 31, TAG)) (1 = +1);
+ *   priority(t):   bits 31..24 = bit b of planes j = 0..7 (plane 0 = MSB),
+ *                  plane j = word (j & 3) of Philox(key, (wi, t, j >> 2, TAG));
+ *                  bits 23..0 = word (b & 3) of Philox(key, (wi, t, 2 + (b >> 2), TAG)) >> 8;
+ *   uniform(t):    the same with q = 10 + (j >> 2) for the planes and
+ *                  q = 12 + (b >> 2) for the low bits;
+ *   accept Delta < 0 iff uniform * 2^-32 < exp(Delta / T_t).
+ * The GPU engine runs the same order level by level and recovers the
+ * best-so-far of this sequential scan exactly (rscan2.cu). */
+#define RS_TAG 5u
+
 typedef struct {
     uint32_t p;
     int32_t v;
@@ -521,66 +529,73 @@ static int prio_cmp(const void *a, const void *b) {
     return x->v < y->v ? -1 : (x->v > y->v);
 }
 
-static uint32_t philox_word(const uint32_t key[2], uint32_t c0, uint32_t c1, uint32_t c2,
-                            uint32_t c3, int word) {
-    uint32_t ctr[4] = {c0, c1, c2, c3}, o[4];
-    gso_philox4x32_10(ctr, key, o);
-    return o[word];
+/* The 32 Philox values of word wi at sweep t (one per bit b): bits 31..24 from
+ * the planes of blocks q0, q0+1, bits 23..0 from word (b & 3) of block
+ * q0 + 2 + (b >> 2), shifted right by 8. */
+static void rs_values(const uint32_t key[2], uint32_t wi, uint32_t t, uint32_t q0,
+                      uint32_t out[32]) {
+    uint32_t pl[8], o[4];
+    for (uint32_t g = 0; g < 2; g++) {
+        uint32_t ctr[4] = {wi, t, q0 + g, RS_TAG};
+        gso_philox4x32_10(ctr, key, o);
+        for (int j = 0; j < 4; j++) pl[4 * g + j] = o[j];
+    }
+    for (int b = 0; b < 32; b++) {
+        uint32_t hi = 0;
+        for (int j = 0; j < 8; j++) hi |= ((pl[j] >> b) & 1u) << (31 - j);
+        out[b] = hi;
+    }
+    for (uint32_t g = 0; g < 8; g++) {
+        uint32_t ctr[4] = {wi, t, q0 + 2u + g, RS_TAG};
+        gso_philox4x32_10(ctr, key, o);
+        for (int j = 0; j < 4; j++) out[4 * g + j] |= o[j] >> 8;
+    }
 }
 
 static int trial_rscan(int32_t rows, int32_t cols, const int8_t *w, const int32_t *eu,
                        const int32_t *ev, const int64_t *ew, int kind, int32_t sweeps,
                        uint64_t seed, double t0, double t1, int64_t *best_cut,
                        int8_t *best_spins, int32_t *sweeps_executed) {
-    int32_t n = rows * cols;
+    int32_t n = rows * cols, WPR = (cols + 31) / 32;
     int64_t m = 2 * (int64_t)n;
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     int8_t *s = (int8_t *)malloc((size_t)n);
     int8_t *bs = (int8_t *)malloc((size_t)n);
     prio_t *pr = (prio_t *)malloc(sizeof(prio_t) * (size_t)n);
-    uint32_t *pv = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n);
-    int32_t *lvl = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
-    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
-    int32_t *cnt = (int32_t *)malloc(sizeof(int32_t) * ((size_t)n + 2));
     int32_t *flog = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
-    for (int32_t v = 0; v < n; v++)
-        s[v] = (philox_word(key, (uint32_t)(v >> 2), 0u, 0u, 3u, v & 3) >> 31) ? 1 : -1;
-    int64_t current = gso_cut(m, eu, ev, ew, s);
-    int64_t best = current;
+    int32_t nwords = rows * WPR;
+    uint32_t *uval = (uint32_t *)malloc(sizeof(uint32_t) * 32 * (size_t)nwords);
+    int32_t *ustamp = (int32_t *)malloc(sizeof(int32_t) * (size_t)nwords);
+    uint32_t vals[32];
+    for (int32_t v = 0; v < n; v++) {
+        int32_t r = v / cols, c = v % cols;
+        uint32_t ctr[4] = {(uint32_t)(r * WPR + (c >> 5)), 0u, 31u, RS_TAG}, o[4];
+        gso_philox4x32_10(ctr, key, o);
+        s[v] = ((o[0] >> (c & 31)) & 1u) ? 1 : -1;
+    }
+    int64_t current = gso_cut(m, eu, ev, ew, s); /* solvers.py:101 */
+    int64_t best = current;                      /* solvers.py:102-103 */
     memcpy(bs, s, (size_t)n);
     int32_t executed = 0;
     int annealing = kind == GSO_ANNEALING;
     for (int32_t sweep = 0; sweep < sweeps; sweep++) {
         double temp = annealing ? gso_temperature(sweeps, t0, t1, sweep) : 0.0;
-        /* priorities, levels (sequential in priority order), visit order */
-        for (int32_t v = 0; v < n; v++) {
-            pv[v] = philox_word(key, (uint32_t)(v >> 2), (uint32_t)sweep, 0u, 4u, v & 3);
-            pr[v].p = pv[v];
-            pr[v].v = v;
+        /* the sweep's order (solvers.py:110): sites sorted by (priority, id) */
+        for (int32_t wi = 0; wi < nwords; wi++) {
+            int32_t r = wi / WPR, c0 = 32 * (wi % WPR);
+            rs_values(key, (uint32_t)wi, (uint32_t)sweep, 0u, vals);
+            for (int b = 0; b < 32 && c0 + b < cols; b++) {
+                int32_t v = r * cols + c0 + b;
+                pr[v].p = vals[b];
+                pr[v].v = v;
+            }
+            ustamp[wi] = -1;
         }
         qsort(pr, (size_t)n, sizeof(prio_t), prio_cmp);
-        int32_t maxl = 0;
-        for (int32_t i = 0; i < n; i++) {
-            int32_t v = pr[i].v, r = v / cols, c = v % cols;
-            int32_t nb[4] = {((r + rows - 1) % rows) * cols + c, ((r + 1) % rows) * cols + c,
-                             r * cols + (c + cols - 1) % cols, r * cols + (c + 1) % cols};
-            int32_t L = 0;
-            for (int d = 0; d < 4; d++) {
-                int32_t u = nb[d];
-                if (pv[u] < pv[v] || (pv[u] == pv[v] && u < v))
-                    if (lvl[u] > L) L = lvl[u];
-            }
-            lvl[v] = L + 1;
-            if (L + 1 > maxl) maxl = L + 1;
-        }
-        for (int32_t l = 0; l <= maxl + 1; l++) cnt[l] = 0;
-        for (int32_t v = 0; v < n; v++) cnt[lvl[v] + 1]++;
-        for (int32_t l = 1; l <= maxl + 1; l++) cnt[l] += cnt[l - 1];
-        for (int32_t v = 0; v < n; v++) order[cnt[lvl[v]]++] = v; /* (lvl, v) */
         int flipped = 0;
         int64_t nlog = 0, nbest = -1;
-        for (int32_t i = 0; i < n; i++) {
-            int32_t v = order[i], r = v / cols, c = v % cols;
+        for (int32_t i = 0; i < n; i++) { /* solvers.py:111-127 */
+            int32_t v = pr[i].v, r = v / cols, c = v % cols;
             int32_t cl = (c + cols - 1) % cols, cr = (c + 1) % cols;
             int32_t ru = (r + rows - 1) % rows, rd = (r + 1) % rows;
             int64_t delta = (int64_t)w[2 * v] * s[r * cols + cr] +
@@ -592,7 +607,12 @@ static int trial_rscan(int32_t rows, int32_t cols, const int8_t *w, const int32_
             if (annealing) {
                 accept = delta >= 0;
                 if (!accept) {
-                    uint32_t u = philox_word(key, (uint32_t)(v >> 2), (uint32_t)sweep, 1u, 4u, v & 3);
+                    int32_t wi = r * WPR + (c >> 5);
+                    if (ustamp[wi] != sweep) {
+                        rs_values(key, (uint32_t)wi, (uint32_t)sweep, 10u, uval + 32 * (size_t)wi);
+                        ustamp[wi] = sweep;
+                    }
+                    uint32_t u = uval[32 * (size_t)wi + (c & 31)];
                     accept = (double)u * (1.0 / 4294967296.0) < exp((double)delta / temp);
                 }
             } else {
@@ -621,7 +641,7 @@ static int trial_rscan(int32_t rows, int32_t cols, const int8_t *w, const int32_
     *best_cut = best;
     if (best_spins) memcpy(best_spins, bs, (size_t)n);
     *sweeps_executed = executed;
-    free(s); free(bs); free(pr); free(pv); free(lvl); free(order); free(cnt); free(flog);
+    free(s); free(bs); free(pr); free(flog); free(uval); free(ustamp);
     return rc;
 }
 

@@ -24,8 +24,10 @@
  *      the trial seed).  DESIGN.md section "Checkerboard contract" is the
  *      normative statement; this file is its executable form.
  *
- *  (3) "random scan" (Philox): the reference's random-order sweep, the order
- *      drawn as Philox priorities and executed level by level -- the
+ *  (3) "random scan" (Philox): solvers.py:107-127 unchanged -- a fresh
+ *      uniformly random visit order every sweep, scanned sequentially --
+ *      with the permutation drawn as i.i.d. 32-bit Philox priorities (sites
+ *      sorted by (priority, id)) and the acceptance uniforms from Philox: the
  *      reference's dynamics in law.
  */
 #ifndef GSB_ORACLE_H

@@ -16,7 +16,7 @@ LIB = PKG / "libgsb_cuda.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "checker_cluster.cu", "refexact.cu", "refexact_warp.cu",
-           "evaluate.cu", "rscan.cu", "rscan_bs.cu"]
+           "evaluate.cu", "rscan2.cu"]
 HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh"]
 
 NVCC_FLAGS = [

@@ -199,7 +199,7 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   int *err = (int *)ws;
   char *rest = (char *)ws + err_bytes();
   size_t rest_bytes = ws_bytes - err_bytes();
-  if (cudaMemsetAsync(err, 0, 16, stream) != cudaSuccess)
+  if (cudaMemsetAsync(err, 0, 64, stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
   int rc;
   if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
@@ -221,14 +221,9 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     } else {
       return set_error(GSB_EUNSUPPORTED, "torus too large for the checkerboard engines");
     }
-  } else if (engine == GSB_ENGINE_RANDOM_SCAN && !getenv("GSB_RSCAN_SCALAR") &&
-             rscan_bs_fits(inst->rows, inst->cols)) {
-    // bit-sliced rounds; the per-site kernel (same results) is the fallback
-    rc = rscan_bs_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
-                      sweeps_exec, best_bits, err, stream);
   } else if (engine == GSB_ENGINE_RANDOM_SCAN) {
-    rc = rscan_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
-                   sweeps_exec, best_bits, err, stream);
+    rc = rscan2_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
+                    sweeps_exec, best_bits, err, (unsigned long long *)((char *)err + 16), stream);
   } else if (engine == GSB_ENGINE_REFERENCE && ref_warp_fits(inst->rows, inst->cols)) {
     rc = ref_warp_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
                       sweeps_exec, best_bits, rest, err, stream);
@@ -241,8 +236,25 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   return rc;
 }
 
-int gsb_rscan_fits(int32_t rows, int32_t cols) {
-  return rscan_bs_fits(rows, cols) || rscan_fits(rows, cols) ? 1 : 0;
+int gsb_rscan_fits(int32_t rows, int32_t cols) { return rscan2_fits(rows, cols) ? 1 : 0; }
+
+int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32_t *rows_per_lane) {
+  if (!warps || !rows_per_lane) return set_error(GSB_EINVAL, "null argument");
+  int nw = 0, rb = 0;
+  if (!rscan2_shape(rows, cols, T, &nw, &rb))
+    return set_error(GSB_EUNSUPPORTED, "torus too large for the random-scan engine");
+  *warps = nw;
+  *rows_per_lane = rb;
+  return GSB_OK;
+}
+
+int gsb_workspace_rscan_stats(const void *ws, void *stream, uint64_t *out4) {
+  if (!ws || !out4) return set_error(GSB_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(out4, (const char *)ws + 16, 32, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return set_error(GSB_ECUDA, cudaGetErrorString(cudaGetLastError()));
+  return GSB_OK;
 }
 
 int gsb_workspace_counters(const void *ws, void *stream, uint64_t *philox_blocks) {

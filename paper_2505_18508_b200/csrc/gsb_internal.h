@@ -39,16 +39,13 @@ int checker_cluster_run(int rows, int cols, const int8_t *w_dev, int kind, int s
                         int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                         cudaStream_t stream);
 
-// random-scan engine (rscan.cu)
-bool rscan_fits(int rows, int cols);
-int rscan_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
-              const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
-              int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws, cudaStream_t stream);
-
-bool rscan_bs_fits(int rows, int cols);
-int rscan_bs_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
-                 const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
-                 int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws, cudaStream_t stream);
+// random-scan engine (rscan2.cu)
+bool rscan2_fits(int rows, int cols);
+bool rscan2_shape(int rows, int cols, int T, int *nw, int *rb);
+int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+               const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
+               int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws,
+               unsigned long long *stats, cudaStream_t stream);
 
 // reference-exact engines (refexact.cu: any graph; refexact_warp.cu: tori, n < 2^16)
 bool ref_warp_fits(int rows, int cols);

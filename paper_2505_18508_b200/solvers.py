@@ -168,8 +168,17 @@ def _graph_dmax(instance: ProblemInstance) -> int:
 
 
 def rscan_fits(rows: int, cols: int) -> bool:
-    """Whether a rows x cols torus fits the random-scan engine (one SM's shared memory)."""
+    """Whether a rows x cols torus fits the random-scan engine (register-resident teams)."""
     return _lib.lib().gsb_rscan_fits(rows, cols) == 1
+
+
+def rscan_shape(rows: int, cols: int, T: int) -> tuple[int, int]:
+    """(warps per trial, rows per lane) the random-scan engine launches for T trials."""
+    import ctypes
+
+    nw, rb = ctypes.c_int32(0), ctypes.c_int32(0)
+    _lib.check(_lib.lib().gsb_rscan_shape(rows, cols, T, ctypes.byref(nw), ctypes.byref(rb)))
+    return nw.value, rb.value
 
 
 def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, device=None,

@@ -236,70 +236,78 @@ def test_random_scan_contract_agrees_in_law_with_reference(oracle):
     assert c.mean() - a.mean() > 4 * se
 
 
-def test_random_scan_oracle_matches_python_restatement(oracle):
-    """Pure-Python restatement of the random-scan contract on small tori: the
-    oracle's (best_cut, best spins) equal it, and every sweep's level-by-level
-    order leaves the same spins as the sequential scan in priority order (the
-    identity the contract rests on)."""
+def _rscan_twin(oracle, R, C, w, annealing, S, seed, t0, t1):
+    """Pure-Python restatement of the random-scan contract (the
+    executable form is oracle/gsb_oracle.c:trial_rscan): solvers.py:91-140
+    line by line, the permutation of sweep t = sites sorted by (priority, id),
+    priorities / uniforms / initial spins from Philox4x32-10."""
     import math
 
+    w = [int(x) for x in w]
+    n, WPR = R * C, (C + 31) // 32
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+
+    def value(wi, t, q0, b):  # bits 31..24 from the planes, 23..0 per site
+        hi = 0
+        for g in range(2):
+            o = oracle.philox([wi, t, q0 + g, 5], key)
+            for j in range(4):
+                hi |= ((o[j] >> b) & 1) << (31 - 4 * g - j)
+        return hi | (oracle.philox([wi, t, q0 + 2 + (b >> 2), 5], key)[b & 3] >> 8)
+
+    def wb(v):
+        r, c = divmod(v, C)
+        return r * WPR + (c >> 5), c & 31
+
+    nb = []
+    for v in range(n):
+        r, c = divmod(v, C)
+        nb.append((((r - 1) % R) * C + c, ((r + 1) % R) * C + c, r * C + (c - 1) % C,
+                   r * C + (c + 1) % C))
+
+    def cut(sp):
+        return sum(w[2 * v] * (sp[v] != sp[nb[v][3]]) + w[2 * v + 1] * (sp[v] != sp[nb[v][1]])
+                   for v in range(n))
+
+    sp = []
+    for v in range(n):
+        wi, b = wb(v)
+        sp.append(1 if (oracle.philox([wi, 0, 31, 5], key)[0] >> b) & 1 else -1)  # solvers.py:96
+    cur = best = cut(sp)                                                         # :101-103
+    bsp, executed = list(sp), 0
+    for t in range(S):                                                           # :107
+        T = (t0 if S == 1 else t0 * (t1 / t0) ** (t / (S - 1))) if annealing else None
+        order = sorted(range(n), key=lambda v: (value(wb(v)[0], t, 0, wb(v)[1]), v))  # :110
+        flipped = False
+        for v in order:                                                          # :111-127
+            up, dn, lf, rt = nb[v]
+            d = sp[v] * (w[2 * v] * sp[rt] + w[2 * v + 1] * sp[dn] + w[2 * lf] * sp[lf] +
+                         w[2 * up + 1] * sp[up])
+            if annealing:
+                acc = d >= 0 or value(wb(v)[0], t, 10, wb(v)[1]) / 2**32 < math.exp(d / T)
+            else:
+                acc = d > 0
+            if acc:
+                sp[v], cur, flipped = -sp[v], cur + d, True
+                if cur > best:
+                    best, bsp = cur, list(sp)
+        executed = t + 1
+        if not annealing and not flipped:
+            break
+    return best, bsp, executed
+
+
+def test_random_scan_oracle_matches_python_restatement(oracle):
+    """The C oracle of the random-scan contract equals the pure-Python
+    restatement (best cut, best spins, sweeps executed) on small tori, both
+    kinds, including a torus wider than one 32-site word."""
     from paper_2505_18508_b200.campaign import mix_seeds
 
-    for (R, C, s) in [(3, 3, 1), (4, 5, 2), (6, 7, 3)]:
-        w = [int(x) for x in oracle.torus_weights(R, C, s)]
-        n = R * C
-        nbrs = []
-        for v in range(n):
-            r, c = divmod(v, C)
-            nbrs.append((((r - 1) % R) * C + c, ((r + 1) % R) * C + c, r * C + (c - 1) % C,
-                         r * C + (c + 1) % C))
-
-        def delta(v, sp):
-            up, dn, lf, rt = nbrs[v]
-            return sp[v] * (w[2 * v] * sp[rt] + w[2 * v + 1] * sp[dn] + w[2 * lf] * sp[lf] +
-                            w[2 * up + 1] * sp[up])
-
-        def cut(sp):
-            return sum(w[2 * v] * (sp[v] != sp[nbrs[v][3]]) + w[2 * v + 1] * (sp[v] != sp[nbrs[v][1]])
-                       for v in range(n))
-
-        for seed in mix_seeds(7, range(3)):
-            seed = int(seed)
-            key = [seed & 0xFFFFFFFF, seed >> 32]
-
-            def ph(q, t, a, b, i):
-                return oracle.philox([q, t, a, b], key)[i]
-
-            sp = [1 if ph(v >> 2, 0, 0, 3, v & 3) >> 31 else -1 for v in range(n)]
-            S, t0, t1 = 6, 3.0, 0.05
-            cur = best = cut(sp)
-            bsp = list(sp)
-            for t in range(S):
-                T = t0 * (t1 / t0) ** (t / (S - 1))
-                pr = [ph(v >> 2, t, 0, 4, v & 3) for v in range(n)]
-                u = [ph(v >> 2, t, 1, 4, v & 3) for v in range(n)]
-
-                def visit(v, st):
-                    d = delta(v, st)
-                    if d >= 0 or u[v] / 2**32 < math.exp(d / T):
-                        st[v] = -st[v]
-                        return d
-                    return None
-
-                seq = list(sp)
-                by_prio = sorted(range(n), key=lambda v: (pr[v], v))
-                for v in by_prio:
-                    visit(v, seq)
-                lvl = [0] * n
-                for v in by_prio:
-                    lvl[v] = 1 + max([lvl[x] for x in nbrs[v] if (pr[x], x) < (pr[v], v)] or [0])
-                for v in sorted(range(n), key=lambda v: (lvl[v], v)):
-                    d = visit(v, sp)
-                    if d is not None:
-                        cur += d
-                        if cur > best:
-                            best, bsp = cur, list(sp)
-                assert sp == seq, (R, C, seed, t)
-            bc, bs, _ = oracle.run_trials_rscan(R, C, oracle.torus_weights(R, C, s),
-                                                "simulated_annealing_random_scan", S, [seed], t0, t1)
-            assert int(bc[0]) == best and [int(x) for x in bs[0]] == bsp, (R, C, seed)
+    for (R, C, s) in [(3, 3, 1), (4, 5, 2), (6, 7, 3), (3, 40, 4)]:
+        w = oracle.torus_weights(R, C, s)
+        for seed in [int(x) for x in mix_seeds(7, range(2))] + [2**64 - 1]:
+            for kind, S, t0, t1 in [("simulated_annealing_random_scan", 6, 3.0, 0.05),
+                                    ("greedy_random_scan", 20, 0.0, 0.0)]:
+                want = _rscan_twin(oracle, R, C, w, kind.startswith("sim"), S, seed, t0, t1)
+                bc, bs, se = oracle.run_trials_rscan(R, C, w, kind, S, [seed], t0, t1)
+                assert (int(bc[0]), [int(x) for x in bs[0]], int(se[0])) == want, (R, C, seed, kind)
