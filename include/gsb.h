@@ -58,7 +58,7 @@ extern "C" {
 #define GSB_ENGINE_RANDOM_SCAN 4  /* Philox4x32-10 + the reference's random visit order
                                      (i.i.d. 32-bit priorities, DESIGN.md random-scan contract):
                                      solvers.py:107-127 with the same law, best-so-far of the
-                                     sequential scan exact; tori up to 4 warps x 13 rows per lane */
+                                     sequential scan exact; tori up to 8 warps x 7 rows per lane */
 
 typedef struct gsb_torus {
     int32_t rows, cols;  /* TorusSpec.rows/cols (instances.py:186-187), >= 3 */
@@ -117,13 +117,24 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
                     void *workspace_dev, size_t workspace_bytes, void *stream);
 
 /* 1 if a rows x cols torus fits the random-scan engine (GSB_ENGINE_RANDOM_SCAN:
- * cols <= 1024 and rows <= 4 * floor(32 / ceil(cols / 32)) * 13), else 0. */
+ * cols <= 1024 and rows <= 8 * floor(32 / ceil(cols / 32)) * 7), else 0. */
 int gsb_rscan_fits(int32_t rows, int32_t cols);
 
 /* Team shape the random-scan engine launches for T trials of a rows x cols
  * torus (one CTA of *warps warps per trial, *rows_per_lane rows per lane);
  * needs a device (SM count).  Introspection for tests and profiles. */
 int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32_t *rows_per_lane);
+
+/* TEST-ONLY: force the team shape (warps per trial, rows per lane) of later
+ * random-scan launches of this process, so parity tests can reach every kernel
+ * instantiation at small trial counts; (0, 0) restores the automatic choice.
+ * A shape that cannot hold the torus makes the sweep return GSB_EUNSUPPORTED. */
+int gsb_test_rscan_shape(int32_t warps, int32_t rows_per_lane);
+
+/* TEST-ONLY: shrink the random-scan engine's tie queue and step-4b event list
+ * (0 = default) so parity tests reach their overflow paths (ties decided by
+ * the owning lane, candidate buckets split over passes, ordered extraction). */
+int gsb_test_rscan_limits(int32_t tie_queue_cap, int32_t list_cap);
 
 /* Counters of the last random-scan sweep call on this workspace: out4[0] =
  * rounds (summed over trials), [1] sweeps whose best-so-far needed the bucket

@@ -85,6 +85,8 @@ def lib():
         L.gsb_workspace_counters.argtypes = [P, P, P]
         L.gsb_workspace_rscan_stats.argtypes = [P, P, P]
         L.gsb_rscan_shape.argtypes = [i32, i32, i32, P, P]
+        L.gsb_test_rscan_shape.argtypes = [i32, i32]
+        L.gsb_test_rscan_limits.argtypes = [i32, i32]
         L.gsb_philox_bench.argtypes = [i64, P, P]
         L.gsb_best_key.argtypes = [P, i32, i64, P, P]
         if L.gsb_abi_version() != 1:

@@ -16,8 +16,8 @@ LIB = PKG / "libgsb_cuda.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "checker_cluster.cu", "refexact.cu", "refexact_warp.cu",
-           "evaluate.cu", "rscan2.cu"]
-HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh"]
+           "evaluate.cu", "rscan2.cu", "rscan2_nw1.cu", "rscan2_nw2.cu", "rscan2_nw4.cu", "rscan2_nw8.cu"]
+HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh", "rscan2_kernel.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -43,38 +43,49 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          extra_flags: tuple[str, ...] = ()) -> Path:
+    """Compile the library; ``out``/``extra_flags`` build a development variant
+    (e.g. -DGSB_RS2_PROF) next to the shipped one without touching it."""
+    if out is None and not force and not _stale():
         return LIB
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = PKG / "build" / (out.stem if out is not None else "")
+    objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     procs = []
     for s in SOURCES:
         o = objdir / (Path(s).stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / s), "-o", str(o)]
+        cmd = [nvcc(), *NVCC_FLAGS, *extra_flags, "-I", str(INCLUDE), "-c", str(CSRC / s), "-o", str(o)]
         if verbose:
             print(" ".join(cmd))
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), s))
         objs.append(str(o))
     failed = []
     for p, s in procs:
-        out, _ = p.communicate()
+        log, _ = p.communicate()
         if p.returncode != 0:
-            failed.append((s, out.decode()))
-        elif verbose and out:
-            print(out.decode())
+            failed.append((s, log.decode()))
+        elif verbose and log:
+            print(log.decode())
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB.with_suffix(".so.tmp")
+    target = out if out is not None else LIB
+    tmp = target.with_suffix(".so.tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
            *objs, "-Xcompiler", "-fPIC"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    if "--variant" in sys.argv:  # python -m ...build --variant NAME -DFLAG ...
+        i = sys.argv.index("--variant")
+        vdir = PKG.parent / "build_variants"
+        vdir.mkdir(exist_ok=True)
+        print(build(out=vdir / f"libgsb_{sys.argv[i + 1]}.so", extra_flags=tuple(sys.argv[i + 2:]),
+                    verbose="-v" in sys.argv))
+    else:
+        build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+        print(LIB)

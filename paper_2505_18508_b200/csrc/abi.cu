@@ -199,7 +199,7 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   int *err = (int *)ws;
   char *rest = (char *)ws + err_bytes();
   size_t rest_bytes = ws_bytes - err_bytes();
-  if (cudaMemsetAsync(err, 0, 64, stream) != cudaSuccess)
+  if (cudaMemsetAsync(err, 0, 128, stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
   int rc;
   if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
@@ -245,6 +245,19 @@ int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32
     return set_error(GSB_EUNSUPPORTED, "torus too large for the random-scan engine");
   *warps = nw;
   *rows_per_lane = rb;
+  return GSB_OK;
+}
+
+int gsb_test_rscan_shape(int32_t warps, int32_t rows_per_lane) {
+  if ((warps == 0) != (rows_per_lane == 0) || warps < 0 || rows_per_lane < 0)
+    return set_error(GSB_EINVAL, "bad team shape");
+  rscan2_force_shape(warps, rows_per_lane);
+  return GSB_OK;
+}
+
+int gsb_test_rscan_limits(int32_t tie_queue_cap, int32_t list_cap) {
+  if (tie_queue_cap < 0 || list_cap < 0) return set_error(GSB_EINVAL, "bad limits");
+  rscan2_test_limits(tie_queue_cap, list_cap);
   return GSB_OK;
 }
 

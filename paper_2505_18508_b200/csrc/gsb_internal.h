@@ -42,6 +42,8 @@ int checker_cluster_run(int rows, int cols, const int8_t *w_dev, int kind, int s
 // random-scan engine (rscan2.cu)
 bool rscan2_fits(int rows, int cols);
 bool rscan2_shape(int rows, int cols, int T, int *nw, int *rb);
+void rscan2_force_shape(int nw, int rb);
+void rscan2_test_limits(int tqcap, int lcap);
 int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
                int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws,

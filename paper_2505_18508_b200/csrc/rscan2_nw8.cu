@@ -1,0 +1,8 @@
+// rscan2_nw8.cu -- random-scan kernels for teams of 8 warps per trial
+// (template: rscan2_kernel.cuh; one translation unit per team size so the
+// instantiations compile in parallel).
+#include "rscan2_kernel.cuh"
+
+namespace gsb {
+RS2_DEFINE_TABLE(8)
+}  // namespace gsb

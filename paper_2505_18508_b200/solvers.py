@@ -181,6 +181,16 @@ def rscan_shape(rows: int, cols: int, T: int) -> tuple[int, int]:
     return nw.value, rb.value
 
 
+def _test_rscan_shape(warps: int = 0, rows_per_lane: int = 0) -> None:
+    """TEST-ONLY: force the random-scan team shape of later launches ((0, 0) = automatic)."""
+    _lib.check(_lib.lib().gsb_test_rscan_shape(warps, rows_per_lane))
+
+
+def _test_rscan_limits(tie_queue_cap: int = 0, list_cap: int = 0) -> None:
+    """TEST-ONLY: shrink the random-scan tie queue / event list (0 = default)."""
+    _lib.check(_lib.lib().gsb_test_rscan_limits(tie_queue_cap, list_cap))
+
+
 def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, device=None,
                       stream=None, check: bool = True, engine: int | None = None):
     """Batched trials with device-resident outputs (torch tensors).

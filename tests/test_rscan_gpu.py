@@ -40,6 +40,8 @@ from paper_2505_18508_b200.solvers import (  # noqa: E402
     GREEDY_RANDOM_SCAN,
     SolverConfig,
     default_config,
+    _test_rscan_limits,
+    _test_rscan_shape,
     rscan_shape,
     run_trials,
     run_trials_device,
@@ -76,27 +78,44 @@ def test_random_scan_engine_matches_oracle(oracle, R, C, s):
 
 
 def test_random_scan_every_team_shape(oracle):
-    """Every (warps, rows per lane) instantiation, selected through the trial
-    count and torus height, against the oracle on sampled trials."""
-    seen = set()
-    cases = [(3, 8, 1), (5, 200, 2000), (10, 200, 2000), (19, 200, 2000), (37, 200, 2000),
-             (49, 200, 2000), (5, 200, 1), (9, 200, 2000), (17, 200, 2000), (33, 200, 2000),
-             (57, 200, 2000), (85, 200, 2000), (9, 200, 1), (17, 200, 1), (33, 200, 1),
-             (65, 200, 1), (113, 200, 1), (161, 200, 1), (100, 100, 1024), (100, 140, 4096),
-             (30, 100, 1), (60, 100, 3000), (700, 20, 1), (1500, 8, 1)]
-    for (R, C, T) in cases:
-        try:
-            shape = rscan_shape(R, C, T)
-        except ValueError:
-            continue
-        seen.add(shape)
-        inst = generate_torus(TorusSpec(R, C, R + C))
-        seeds = mix_seeds(MASTER, range(T))
-        idx = sorted({0, T - 1, T // 2, T // 3} | set(range(0, T, max(1, T // 6))))
-        _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, 5, 0), seeds, idx)
-        _check(oracle, inst, default_config(GREEDY_RANDOM_SCAN, 40, 0), seeds, idx)
-    want = {(nw, rb) for nw in (1, 2, 4) for rb in (1, 2, 4, 7, 10, 13)}
-    assert want <= seen, sorted(want - seen)
+    """Every (warps, rows per lane) instantiation, forced through the
+    test-only shape override on tori that fill it, against the oracle."""
+    try:
+        for nw in (1, 2, 4, 8):
+            for rb in (1, 2, 3, 4, 5, 7):
+                for C in (200, 100, 33):  # 7 / 4 / 2 words per row (4, 4 and 1 valid bits in the last)
+                    bpw = 32 // ((C + 31) // 32)
+                    R = nw * bpw * rb - (1 if rb > 1 else 0)
+                    if R * C > 30000:
+                        continue
+                    _test_rscan_shape(nw, rb)
+                    inst = generate_torus(TorusSpec(R, C, R + C))
+                    seeds = mix_seeds(MASTER, range(3))
+                    _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, 5, 0), seeds)
+                    _check(oracle, inst, default_config(GREEDY_RANDOM_SCAN, 40, 0), seeds)
+        # a shape that cannot hold the torus is refused, not silently replaced
+        _test_rscan_shape(1, 1)
+        with pytest.raises(ValueError):
+            run_trials(generate_torus(TorusSpec(100, 100, 1)),
+                       default_config(ANNEALING_RANDOM_SCAN, 2, 0), [1, 2])
+    finally:
+        _test_rscan_shape(0, 0)
+
+
+@pytest.mark.parametrize("tq,lc", [(3, 0), (0, 6), (2, 1), (1000000, 40)])
+def test_random_scan_overflow_paths(oracle, tq, lc):
+    """Tiny tie queue / event list: ties decided by the owning lane, candidate
+    buckets split over several passes, buckets beyond the list visited by
+    ordered extraction -- same results as the oracle."""
+    try:
+        _test_rscan_limits(tq, lc)
+        for (R, C, s) in [(9, 11, 4), (40, 33, 7), (50, 100, 1), (100, 200, 1)]:
+            inst = generate_torus(TorusSpec(R, C, s))
+            seeds = mix_seeds(MASTER, range(4))
+            _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, 12, 0), seeds)
+            _check(oracle, inst, SolverConfig(ANNEALING_RANDOM_SCAN, 6, 0, 0.9, 0.3), seeds)
+    finally:
+        _test_rscan_limits(0, 0)
 
 
 @pytest.mark.parametrize("R,C,T,S", [(50, 100, 100, 200), (100, 100, 1024, 60),
@@ -107,6 +126,7 @@ def test_random_scan_benchmark_shapes(oracle, R, C, T, S):
     inst = generate_torus(TorusSpec(R, C, 1))
     seeds = mix_seeds(20250814, range(T))
     idx = sorted(set(np.linspace(0, T - 1, 16).astype(int).tolist()))
+    assert rscan_shape(R, C, T)[0] in (1, 2, 4, 8)
     _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, S, 0), seeds, idx)
     _check(oracle, inst, default_config(GREEDY_RANDOM_SCAN, 200, 0), seeds, idx)
 
