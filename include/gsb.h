@@ -125,6 +125,15 @@ int gsb_rscan_fits(int32_t rows, int32_t cols);
  * needs a device (SM count).  Introspection for tests and profiles. */
 int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32_t *rows_per_lane);
 
+/* TEST-ONLY: force the checkerboard engine's team shape for later launches of
+ * this process: warps per trial (1, 2, 4, 8, 16; 0 = automatic) and the
+ * one-warp kernel variant (0 = automatic, 1 = 128-register, 2 = the 8-per-SM
+ * variant the engine picks when the trials fill fewer than 8 warps per SM), so
+ * parity tests can run the benchmark's instantiations on a handful of trials.
+ * gsb_test_cluster_size forces the cluster engine's CTA count (0 = automatic). */
+int gsb_test_checker_shape(int32_t warps, int32_t variant);
+int gsb_test_cluster_size(int32_t ctas);
+
 /* TEST-ONLY: force the team shape (warps per trial, rows per lane) of later
  * random-scan launches of this process, so parity tests can reach every kernel
  * instantiation at small trial counts; (0, 0) restores the automatic choice.

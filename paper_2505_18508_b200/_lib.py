@@ -86,6 +86,8 @@ def lib():
         L.gsb_workspace_rscan_stats.argtypes = [P, P, P]
         L.gsb_rscan_shape.argtypes = [i32, i32, i32, P, P]
         L.gsb_test_rscan_shape.argtypes = [i32, i32]
+        L.gsb_test_checker_shape.argtypes = [i32, i32]
+        L.gsb_test_cluster_size.argtypes = [i32]
         L.gsb_test_rscan_limits.argtypes = [i32, i32]
         L.gsb_philox_bench.argtypes = [i64, P, P]
         L.gsb_best_key.argtypes = [P, i32, i64, P, P]

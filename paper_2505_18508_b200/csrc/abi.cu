@@ -248,6 +248,20 @@ int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32
   return GSB_OK;
 }
 
+int gsb_test_checker_shape(int32_t warps, int32_t variant) {
+  if (!(warps == 0 || warps == 1 || warps == 2 || warps == 4 || warps == 8 || warps == 16) ||
+      variant < 0 || variant > 2)
+    return set_error(GSB_EINVAL, "bad checkerboard team shape");
+  checker_force_shape(warps, variant);
+  return GSB_OK;
+}
+
+int gsb_test_cluster_size(int32_t ctas) {
+  if (ctas < 0 || ctas > 16 || (ctas & (ctas - 1))) return set_error(GSB_EINVAL, "bad cluster size");
+  checker_cluster_force_size(ctas);
+  return GSB_OK;
+}
+
 int gsb_test_rscan_shape(int32_t warps, int32_t rows_per_lane) {
   if ((warps == 0) != (rows_per_lane == 0) || warps < 0 || rows_per_lane < 0)
     return set_error(GSB_EINVAL, "bad team shape");

@@ -672,11 +672,21 @@ size_t checker_workspace_bytes(int rows, int cols) {
          align_up((size_t)2 * nw * 32, 256);
 }
 
+// test-only overrides (gsb_test_checker_shape): warps per trial (0 = automatic)
+// and the one-warp variant (0 = automatic, 1 = 128-register, 2 = 8-per-SM 246-register)
+static int g_force_warps = 0, g_force_variant = 0;
+
+void checker_force_shape(int warps, int variant) {
+  g_force_warps = warps;
+  g_force_variant = variant;
+}
+
 template <int WPT>
 static int launch_wpt(const CheckerArgs &a, bool sa, int nsm, int W, cudaStream_t stream) {
   switch (W) {
     case 1:
-      if (a.T <= 8 * nsm && !getenv("GSB_CHECKER_THIN")) return launch_nt<32, WPT, 8>(a, sa, nsm, stream);
+      if (g_force_variant ? g_force_variant == 2 : a.T <= 8 * nsm)
+        return launch_nt<32, WPT, 8>(a, sa, nsm, stream);
       return launch_nt<32, WPT>(a, sa, nsm, stream);
     case 2: return launch_nt<64, WPT>(a, sa, nsm, stream);
     case 4: return launch_nt<128, WPT>(a, sa, nsm, stream);
@@ -720,8 +730,6 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.err = err_ws;
   a.blocks = (unsigned long long *)((char *)err_ws + 8);
   a.zp_max = 8;
-  if (const char *zv = getenv("GSB_CHECKER_ZP"))  // development A/B knob: 0, 4 or 8
-    a.zp_max = atoi(zv);
   const bool sa = kind == GSB_ANNEALING;
   // Team shape: W warps per trial (power of two), WPT <= 8 words per lane.
   // As few warps per trial as possible (a one-warp team needs no CTA barriers
@@ -731,10 +739,11 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   while (W < 16 && 32 * W < nw &&
          ((long long)T * W < 2LL * nsm || (nw + 32 * W - 1) / (32 * W) > 8))
     W *= 2;
-  if (const char *ov = getenv("GSB_CHECKER_WARPS")) {  // development tuning knob
-    const int w = atoi(ov);
-    if ((w == 1 || w == 2 || w == 4 || w == 8 || w == 16) && (nw + 32 * w - 1) / (32 * w) <= 8)
-      W = w;
+  if (g_force_warps) {
+    const int w = g_force_warps;
+    if (!((w == 1 || w == 2 || w == 4 || w == 8 || w == 16) && (nw + 32 * w - 1) / (32 * w) <= 8))
+      return set_error(GSB_EUNSUPPORTED, "forced checkerboard team shape cannot hold the torus");
+    W = w;
   }
   const int wpt = (nw + 32 * W - 1) / (32 * W);
   if (wpt > 8) return set_error(GSB_EUNSUPPORTED, "checkerboard team shape out of range");

@@ -776,6 +776,10 @@ static int cl_run_wpt(int wpt, const ClusterArgs &a, bool sa, int T, cudaStream_
   }
 }
 
+static int g_force_cluster = 0;  // test-only override (gsb_test_cluster_size)
+
+void checker_cluster_force_size(int c) { g_force_cluster = c; }
+
 int checker_cluster_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                         const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
                         int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
@@ -804,10 +808,9 @@ int checker_cluster_run(int rows, int cols, const int8_t *w_dev, int kind, int s
   a.blocks = (unsigned long long *)((char *)err_ws + 8);
   const bool sa = kind == GSB_ANNEALING;
   // cluster size: the one that keeps the most SMs busy with these T trials
-  // (ties -> the smaller cluster); GSB_CLUSTER_SIZE forces one (tests, tuning)
+  // (ties -> the smaller cluster); gsb_test_cluster_size forces one (tests)
   int bestC = 0, bestUsed = -1;
-  int forced = 0;
-  if (const char *ov = getenv("GSB_CLUSTER_SIZE")) forced = atoi(ov);
+  const int forced = g_force_cluster;
   for (int C = 1; C <= CL_MAXC; C *= 2) {
     if (forced && C != forced) continue;
     const int wpt = cluster_wpt(rows, cols, C);

@@ -21,6 +21,9 @@ int checker_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                 int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                 cudaStream_t stream);
 
+void checker_force_shape(int warps, int variant);
+void checker_cluster_force_size(int c);
+
 void checker_masks_kernel_launch(int rows, int cols, int WPR, const int8_t *w, uint4 *masks,
                                  uint4 *geo, cudaStream_t stream);
 // HBM-tiled checkerboard engine (checker_hbm.cu)

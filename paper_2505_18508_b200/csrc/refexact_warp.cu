@@ -499,7 +499,7 @@ int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.inv_cols = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)cols - 1) / (uint64_t)cols);
   a.err = err_ws;
   const size_t smem = ref_warp_smem(n);
-  auto kern = getenv("GSB_REFWARP_V1") ? ref_warp_kernel<false> : ref_warp_kernel<true>;
+  auto kern = ref_warp_kernel<true>;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)

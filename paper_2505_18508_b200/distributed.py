@@ -152,3 +152,48 @@ def run_sharded(instance, config, master_seed: int, num_trials: int, group=None,
     g = reduce_best(best, bits, first, num_trials, group)
     cuts, sw = gather_trials(best, sweeps, num_trials, group)
     return g, cuts, sw
+
+
+def gather_rows(local, counts, group=None):
+    """All-gather a per-trial tensor whose leading dimension is this rank's
+    trial count (counts[r] on rank r) into trial-index order (numpy)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    pad = torch.zeros((max(counts),) + tuple(local.shape[1:]), dtype=local.dtype,
+                      device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return np.concatenate([parts[r][: counts[r]].cpu().numpy() for r in range(world)])
+
+
+def run_sharded_seeds(instance, config, seeds, group=None, device=None):
+    """The multi-GPU form of solvers.run_trials for an explicit seed list (the
+    pending trials of a campaign): rank r runs the r-th contiguous block on
+    its GPU, then every rank receives all results in seed order.  Returns
+    (best_cut, sweeps_executed, hex_of) like a TrialBatch's fields.  Must be
+    called by every rank of the group with the same arguments."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_18508_b200.codec import packed_to_hex
+    from paper_2505_18508_b200.solvers import run_trials_device
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    seeds = np.asarray(seeds, dtype=np.uint64)
+    blocks = [shard(len(seeds), world, r) for r in range(world)]
+    first, count = blocks[rank]
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    best, sweeps, bits = run_trials_device(instance, config, seeds[first:first + count],
+                                           device=device)
+    if dist.get_backend(group) == "gloo":  # CPU collectives (development / tests)
+        best, sweeps, bits = best.cpu(), sweeps.cpu(), bits.cpu()
+    counts = [c for _, c in blocks]
+    cuts = gather_rows(best, counts, group)
+    done = gather_rows(sweeps, counts, group)
+    allbits = gather_rows(bits, counts, group)
+    n = instance.n
+    return cuts, done, lambda j: packed_to_hex(allbits[j], n)

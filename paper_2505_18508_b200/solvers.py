@@ -159,6 +159,16 @@ def schedule_table(config: SolverConfig, dmax: int = 4) -> np.ndarray | None:
     return tab
 
 
+# engines that run the same trial contract (an override may only move inside one)
+_ENGINE_FAMILY = {
+    _lib.ENGINE_REFERENCE: "reference",
+    _lib.ENGINE_CHECKERBOARD: "checkerboard",
+    _lib.ENGINE_CHECKERBOARD_TILED: "checkerboard",
+    _lib.ENGINE_CHECKERBOARD_CLUSTER: "checkerboard",
+    _lib.ENGINE_RANDOM_SCAN: "random_scan",
+}
+
+
 def _graph_dmax(instance: ProblemInstance) -> int:
     eu, ev, ew = instance.edge_arrays()
     tot = np.zeros(instance.n, dtype=np.int64)
@@ -184,6 +194,16 @@ def rscan_shape(rows: int, cols: int, T: int) -> tuple[int, int]:
 def _test_rscan_shape(warps: int = 0, rows_per_lane: int = 0) -> None:
     """TEST-ONLY: force the random-scan team shape of later launches ((0, 0) = automatic)."""
     _lib.check(_lib.lib().gsb_test_rscan_shape(warps, rows_per_lane))
+
+
+def _test_checker_shape(warps: int = 0, variant: int = 0) -> None:
+    """TEST-ONLY: force the checkerboard team shape / one-warp variant (0 = automatic)."""
+    _lib.check(_lib.lib().gsb_test_checker_shape(warps, variant))
+
+
+def _test_cluster_size(ctas: int = 0) -> None:
+    """TEST-ONLY: force the cluster engine's CTA count (0 = automatic)."""
+    _lib.check(_lib.lib().gsb_test_cluster_size(ctas))
 
 
 def _test_rscan_limits(tie_queue_cap: int = 0, list_cap: int = 0) -> None:
@@ -221,11 +241,19 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
         return best, sweeps, bits
     kind = _lib.GSB_ANNEALING if config.annealing else _lib.GSB_GREEDY
     eng = config.engine if engine is None else engine
-    if engine is not None and (engine == _lib.ENGINE_REFERENCE) != (config.engine == _lib.ENGINE_REFERENCE):
-        raise ValueError("engine override must keep the kind's trial semantics")
+    if engine is not None and _ENGINE_FAMILY.get(engine) != _ENGINE_FAMILY[config.engine]:
+        raise ValueError("engine override must keep the kind's trial semantics "
+                         "(checkerboard kinds: CHECKERBOARD / _TILED / _CLUSTER only)")
     with torch.cuda.device(dev):
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        cur = torch.cuda.current_stream(dev)
+        s = stream if stream is not None else cur
         sp = s.cuda_stream
+        if s != cur:
+            # inputs and scratch are produced / allocated on the current stream:
+            # order the launch stream after it and tie their lifetime to `s`
+            s.wait_stream(cur)
+            for t in (seeds_d, best, sweeps, bits):
+                t.record_stream(s)
         if instance.torus is not None:
             w = instance.device_weights(dev)
             ts = _lib.torus_struct(instance.torus.rows, instance.torus.cols, w.data_ptr())
@@ -233,6 +261,10 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
             tab_d = (torch.from_numpy(tab.view(np.int64)).to(dev) if tab is not None else None)
             wsb = L.gsb_torus_workspace_bytes(ts, eng, config.sweeps, T)
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+            if s != cur:
+                s.wait_stream(cur)  # weights / table / workspace just produced on `cur`
+                for t in (w, ws) + ((tab_d,) if tab_d is not None else ()):
+                    t.record_stream(s)
             _lib.check(L.gsb_torus_sweep(ts, eng, kind, config.sweeps,
                                          tab_d.data_ptr() if tab_d is not None else None,
                                          seeds_d.data_ptr(), T, best.data_ptr(),
@@ -250,6 +282,10 @@ def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, de
             tab_d = (torch.from_numpy(tab.view(np.int64)).to(dev) if tab is not None else None)
             wsb = L.gsb_graph_workspace_bytes(gs, config.sweeps, T)
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+            if s != cur:
+                s.wait_stream(cur)
+                for t in (eu, ev, ew, ws) + ((tab_d,) if tab_d is not None else ()):
+                    t.record_stream(s)
             _lib.check(L.gsb_graph_sweep(gs, kind, config.sweeps,
                                          tab_d.data_ptr() if tab_d is not None else None, dmax,
                                          seeds_d.data_ptr(), T, best.data_ptr(),

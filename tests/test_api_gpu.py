@@ -23,7 +23,6 @@ from paper_2505_18508_b200.campaign import (  # noqa: E402
     read_log,
     replay_record,
     run_campaign,
-    sweep_scan,
 )
 from paper_2505_18508_b200.distributed import run_sharded  # noqa: E402
 from paper_2505_18508_b200.evaluate import cut_value, flip_delta_cut, ising_energy  # noqa
@@ -170,15 +169,6 @@ def test_campaign_log_resume_replay(tmp_path):
         replay_record(inst, bad)
 
 
-def test_sweep_scan_greedy_ladder_monotone():
-    inst = generate_torus(TorusSpec(8, 8, 42))
-    cfg = CampaignConfig(inst.name, default_config(GREEDY, 1, 0), 50, MASTER,
-                         sweep_scan=(1, 2, 4, 8))
-    rows = sweep_scan(inst, cfg)
-    hs = [r.highest_cut for r in rows]
-    assert hs == sorted(hs)
-
-
 def test_run_sharded_single_rank_equals_batch():
     inst = generate_torus(TorusSpec(50, 100, 1))
     cfg = default_config(ANNEALING_CHECKERBOARD, 30, 0)
@@ -188,3 +178,41 @@ def test_run_sharded_single_rank_equals_batch():
     i = int(np.argmax(b.best_cut))
     assert (g.best_cut, g.index) == (int(b.best_cut[i]), i)
     assert g.bits.tobytes() == b.bits[i].tobytes()
+
+
+def test_engine_override_stays_inside_the_contract_family():
+    """An engine override may pick another engine of the SAME trial contract
+    only (solvers.run_trials_device): never checkerboard <-> random scan."""
+    from paper_2505_18508_b200 import _lib
+    from paper_2505_18508_b200.solvers import ANNEALING_RANDOM_SCAN
+
+    inst = generate_torus(TorusSpec(8, 8, 1))
+    seeds = [1, 2, 3]
+    a = run_trials(inst, default_config(ANNEALING_CHECKERBOARD, 10, 0), seeds)
+    b = run_trials(inst, default_config(ANNEALING_CHECKERBOARD, 10, 0), seeds,
+                   engine=_lib.ENGINE_CHECKERBOARD_TILED)
+    assert np.array_equal(a.best_cut, b.best_cut) and np.array_equal(a.bits, b.bits)
+    for kind, eng in ((ANNEALING_CHECKERBOARD, _lib.ENGINE_RANDOM_SCAN),
+                      (ANNEALING_RANDOM_SCAN, _lib.ENGINE_CHECKERBOARD),
+                      (ANNEALING_RANDOM_SCAN, _lib.ENGINE_CHECKERBOARD_TILED),
+                      (ANNEALING, _lib.ENGINE_CHECKERBOARD),
+                      (ANNEALING_CHECKERBOARD, _lib.ENGINE_REFERENCE)):
+        with pytest.raises(ValueError, match="engine override"):
+            run_trials(inst, default_config(kind, 10, 0), seeds, engine=eng)
+
+
+def test_run_trials_device_on_a_side_stream():
+    """stream=: inputs made on the current stream are ordered before the launch
+    and kept alive for it (record_stream); results equal the default-stream run."""
+    from paper_2505_18508_b200.solvers import ANNEALING_RANDOM_SCAN, run_trials_device
+
+    inst = generate_torus(TorusSpec(20, 30, 2))
+    seeds = [int(s) for s in np.arange(1, 40)]
+    for kind in (ANNEALING_RANDOM_SCAN, ANNEALING_CHECKERBOARD, ANNEALING):
+        cfg = default_config(kind, 25, 0)
+        ref = run_trials_device(inst, cfg, seeds)
+        side = torch.cuda.Stream()
+        outs = [run_trials_device(inst, cfg, seeds, stream=side, check=False) for _ in range(3)]
+        side.synchronize()
+        for o in outs:
+            assert torch.equal(o[0], ref[0]) and torch.equal(o[2], ref[2])

@@ -24,6 +24,7 @@ from paper_2505_18508_b200.solvers import (  # noqa: E402
     ANNEALING_CHECKERBOARD,
     GREEDY_CHECKERBOARD,
     SolverConfig,
+    _test_cluster_size,
     default_config,
     run_trials,
 )
@@ -39,6 +40,12 @@ def _check(oracle, inst, cfg, seeds, engine=CLUSTER):
     for i in range(len(seeds)):
         assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
             bc[i], se[i], oracle.encode_hex(bs[i])), (R, C, cfg.kind, i)
+
+
+@pytest.fixture(autouse=True)
+def _automatic_cluster_size_afterwards():
+    yield
+    _test_cluster_size(0)
 
 
 # (rows, cols, seed, cluster sizes): words per row WPR = ceil(cols/64) must be a
@@ -57,11 +64,11 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("R,C,s,sizes", SHAPES)
-def test_cluster_engine_matches_oracle(oracle, monkeypatch, R, C, s, sizes):
+def test_cluster_engine_matches_oracle(oracle, R, C, s, sizes):
     inst = generate_torus(TorusSpec(R, C, s))
     seeds = [int(x) for x in mix_seeds(MASTER, range(9))] + [0, 2**64 - 1]
     for cs in sizes:
-        monkeypatch.setenv("GSB_CLUSTER_SIZE", str(cs))
+        _test_cluster_size(cs)
         for cfg in (default_config(ANNEALING_CHECKERBOARD, 25, 0),
                     default_config(GREEDY_CHECKERBOARD, 200, 0),
                     SolverConfig(ANNEALING_CHECKERBOARD, 7, 0, 1e12, 1e11),  # always accept
@@ -69,14 +76,14 @@ def test_cluster_engine_matches_oracle(oracle, monkeypatch, R, C, s, sizes):
             _check(oracle, inst, cfg, seeds)
 
 
-def test_cluster_engine_randomized(oracle, monkeypatch):
+def test_cluster_engine_randomized(oracle):
     rng = np.random.default_rng(99)
     for _ in range(10):
         wpr = int(rng.choice([1, 2, 4, 8]))
         C = int(rng.integers(max(4, 32 * (wpr - 1) + 1), 32 * wpr + 1)) * 2
         R = int(rng.integers(2, 40)) * 2
         cs = int(rng.choice([c for c in (1, 2, 4, 8, 16) if c <= R]))
-        monkeypatch.setenv("GSB_CLUSTER_SIZE", str(cs))
+        _test_cluster_size(cs)
         t0 = float(rng.uniform(0.5, 5.0))
         cfg = SolverConfig(ANNEALING_CHECKERBOARD, int(rng.integers(1, 30)), 0, t0,
                            t0 * float(rng.uniform(0.005, 0.9)))

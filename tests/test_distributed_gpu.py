@@ -54,3 +54,61 @@ def test_nccl_run_sharded_matches_single_device(nccl_world1):
     assert g.best_cut == top
     assert g.index == int(np.nonzero(bc == top)[0][0])  # ties -> lowest trial index
     assert g.bits.tobytes() == bits[g.index].cpu().numpy().tobytes()
+
+
+def _campaign_worker(rank, world, port, log_path, ret):
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    # development arrangement for a one-GPU box: both ranks on cuda:0, CPU
+    # collectives (gloo); the ranks never wait on each other inside a kernel
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    from paper_2505_18508_b200 import TorusSpec, generate_torus
+    from paper_2505_18508_b200.campaign import CampaignConfig, TargetSpec, run_campaign
+    from paper_2505_18508_b200.solvers import ANNEALING_RANDOM_SCAN, default_config
+
+    torch.cuda.set_device(0)
+    inst = generate_torus(TorusSpec(12, 20, 5))
+    cfg = CampaignConfig(inst.name, default_config(ANNEALING_RANDOM_SCAN, 30, 0), 21, 77,
+                         targets=(TargetSpec("t", 150),))
+    s = run_campaign(inst, cfg, log_path=log_path, include_spins=True)
+    if rank == 0:
+        ret.put(s.deterministic_fields())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_run_campaign_shards_over_the_process_group(tmp_path):
+    """run_campaign under a 2-rank process group: each rank runs its block of
+    the pending trials, rank 0 writes the log; summary and log lines equal the
+    single-process campaign's (results never depend on the world size)."""
+    import torch.multiprocessing as mp
+
+    from paper_2505_18508_b200 import TorusSpec, generate_torus
+    from paper_2505_18508_b200.campaign import (CampaignConfig, TargetSpec, read_log,
+                                                run_campaign)
+    from paper_2505_18508_b200.solvers import ANNEALING_RANDOM_SCAN, default_config
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    log2 = tmp_path / "two_ranks.log"
+    procs = [ctx.Process(target=_campaign_worker, args=(r, 2, port, str(log2), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    fields = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    inst = generate_torus(TorusSpec(12, 20, 5))
+    cfg = CampaignConfig(inst.name, default_config(ANNEALING_RANDOM_SCAN, 30, 0), 21, 77,
+                         targets=(TargetSpec("t", 150),))
+    log1 = tmp_path / "one_rank.log"
+    single = run_campaign(inst, cfg, log_path=log1, include_spins=True)
+    assert fields == single.deterministic_fields()
+    strip = lambda recs: [(r.index, r.seed, r.best_cut, r.sweeps_executed, r.spins_hex)  # noqa: E731
+                          for r in recs]
+    assert strip(read_log(log2)) == strip(read_log(log1)) and len(read_log(log2)) == 21

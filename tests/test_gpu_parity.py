@@ -27,6 +27,7 @@ from paper_2505_18508_b200.solvers import (  # noqa: E402
     GREEDY,
     GREEDY_CHECKERBOARD,
     SolverConfig,
+    _test_checker_shape,
     default_config,
     run_trials,
 )
@@ -144,6 +145,72 @@ def test_checkerboard_engine_matches_oracle(oracle, R, C, s):
             assert int(b.best_cut[i]) == bc[i], (cfg.kind, i)
             assert int(b.sweeps_executed[i]) == se[i], (cfg.kind, i)
             assert b.hex(i) == oracle.encode_hex(bs[i]), (cfg.kind, i)
+
+
+def _check_checker(oracle, inst, cfg, seeds, idx=None):
+    R, C = inst.torus.rows, inst.torus.cols
+    b = run_trials(inst, cfg, seeds)
+    idx = range(len(seeds)) if idx is None else idx
+    sub = [int(seeds[i]) for i in idx]
+    bc, bs, se = oracle.run_trials_checker(R, C, inst.torus_weights, cfg.kind, cfg.sweeps, sub,
+                                           cfg.temp_start, cfg.temp_end)
+    for k, i in enumerate(idx):
+        assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+            bc[k], se[k], oracle.encode_hex(bs[k])), (R, C, cfg.kind, i)
+
+
+# the instantiations bench.py launches (checker.cu team-shape rule at the
+# BASELINE trial counts): config 1 <256,1>, config 2 <32,7,1,8> (one warp x 7
+# words, the 8-per-SM variant), config 3 <64,5>, config 4 <64,7>
+BENCH_SHAPES = [(50, 100, 100, 8, 0), (100, 100, 1024, 1, 2), (100, 140, 4096, 2, 0),
+                (100, 200, 8192, 2, 0)]
+
+
+@pytest.mark.parametrize("R,C,T,warps,variant", BENCH_SHAPES)
+def test_checkerboard_benchmark_shapes_forced(oracle, R, C, T, warps, variant):
+    """The benchmark's kernel instantiation, forced through the test-only
+    shape override on 16 trials x 500 sweeps (SA) and greedy, every trial
+    against the oracle."""
+    inst = generate_torus(TorusSpec(R, C, 1))
+    seeds = mix_seeds(20250814, range(16))
+    try:
+        _test_checker_shape(warps, variant)
+        _check_checker(oracle, inst, default_config(ANNEALING_CHECKERBOARD, 500, 0), seeds)
+        _check_checker(oracle, inst, default_config(GREEDY_CHECKERBOARD, 500, 0), seeds)
+    finally:
+        _test_checker_shape(0, 0)
+
+
+@pytest.mark.parametrize("R,C,T,warps,variant", BENCH_SHAPES)
+def test_checkerboard_benchmark_shapes_at_trial_count(oracle, R, C, T, warps, variant):
+    """The launch bench.py makes (automatic team shape at the BASELINE trial
+    count), a sample of 16 trials against the oracle (results never depend on
+    the batch, so a subset is a valid check)."""
+    inst = generate_torus(TorusSpec(R, C, 1))
+    seeds = mix_seeds(20250814, range(T))
+    idx = sorted(set(np.linspace(0, T - 1, 16).astype(int).tolist()))
+    _check_checker(oracle, inst, default_config(ANNEALING_CHECKERBOARD, 60, 0), seeds, idx)
+    _check_checker(oracle, inst, default_config(GREEDY_CHECKERBOARD, 200, 0), seeds, idx)
+
+
+def test_checkerboard_every_words_per_lane(oracle):
+    """Words per lane 1..8 of the one-warp team (both register variants) and
+    of two- and four-warp teams, on tori chosen to fill them."""
+    try:
+        for warps in (1, 2, 4):
+            for wpt in range(1, 9):
+                nwords = 32 * warps * wpt  # words per colour
+                rows = 2 * max(2, nwords // 4 // 2)  # 4 words per row (cols = 250 -> H = 125)
+                inst = generate_torus(TorusSpec(rows, 250, wpt + warps))
+                seeds = mix_seeds(MASTER, range(5))
+                for variant in ((1, 2) if warps == 1 else (0,)):
+                    _test_checker_shape(warps, variant)
+                    try:
+                        _check_checker(oracle, inst, default_config(ANNEALING_CHECKERBOARD, 20, 0), seeds)
+                    except ValueError:
+                        continue  # this torus does not fit the forced shape
+    finally:
+        _test_checker_shape(0, 0)
 
 
 def test_checkerboard_batch_invariance():
