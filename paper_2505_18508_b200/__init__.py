@@ -5,7 +5,7 @@ problem construction, run_trial / run_campaign and TrialResult, backed by
 hand-written sm_100a CUDA kernels in libgsb_cuda.so (include/gsb.h).
 """
 
-from paper_2505_18508_b200.codec import decode_hex, encode_hex, global_flip
+from paper_2505_18508_b200.codec import decode_hex, encode_hex
 from paper_2505_18508_b200.instances import (
     GsetFormatError,
     ProblemInstance,
@@ -24,7 +24,6 @@ __all__ = [
     "parse_torus_name",
     "decode_hex",
     "encode_hex",
-    "global_flip",
 ]
 
 __version__ = "0.1.0"

@@ -71,25 +71,3 @@ def packed_to_hex(packed: np.ndarray, n: int) -> str:
 def unpack_spins(packed: np.ndarray, n: int) -> np.ndarray:
     bits = np.unpackbits(np.asarray(packed, dtype=np.uint8))[:n]
     return np.where(bits == 1, 1, -1).astype(np.int8)
-
-
-def global_flip(spins) -> tuple[int, ...]:
-    """codec.py:86-88."""
-    return tuple(-s for s in spins)
-
-
-def strip_solution_text(text: str) -> str:
-    return "\n".join(line for line in text.splitlines() if not line.lstrip().startswith("#"))
-
-
-def read_solution_header(text: str) -> dict[str, str]:
-    meta: dict[str, str] = {}
-    for line in text.splitlines():
-        stripped = line.lstrip()
-        if not stripped.startswith("#"):
-            break
-        for tok in stripped[1:].split():
-            if "=" in tok:
-                k, v = tok.split("=", 1)
-                meta[k] = v
-    return meta

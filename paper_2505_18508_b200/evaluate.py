@@ -1,4 +1,5 @@
-"""Exact evaluation (mirror of gsetbench.evaluate, evaluate.py:1-111).
+"""Exact evaluation (mirror of gsetbench.evaluate: cut_value, ising_energy,
+flip_delta_cut, evaluate.py:35-64).
 
 ``cut_value`` / ``ising_energy`` run on the GPU evaluator
 (gsb_torus_cut_energy / gsb_graph_cut_energy); ``*_batch`` evaluates many
@@ -6,8 +7,6 @@ packed bitstrings in one launch.
 """
 
 from __future__ import annotations
-
-from dataclasses import dataclass
 
 import numpy as np
 
@@ -81,37 +80,3 @@ def flip_delta_cut(instance: ProblemInstance, spins, k: int) -> int:
     for j, w in instance.adjacency[k]:
         acc += w * spins[j - 1]
     return sk * acc
-
-
-def solution_quality(cut: int, best_known: int) -> float:
-    if best_known <= 0:
-        raise ValueError(f"best known cut must be positive, got {best_known}")
-    return cut / best_known
-
-
-def format_quality_percent(quality: float) -> str:
-    return f"{quality * 100:.3f}%"
-
-
-@dataclass(frozen=True)
-class EvaluationReport:
-    instance: str
-    n: int
-    cut: int
-    energy: int
-    quality: float | None = None
-
-    def to_kv(self) -> str:
-        parts = [f"instance={self.instance}", f"n={self.n}", f"cut={self.cut}",
-                 f"energy={self.energy}"]
-        if self.quality is not None:
-            parts.append(f"quality={format_quality_percent(self.quality)}")
-        return " ".join(parts)
-
-
-def evaluate_solution(instance: ProblemInstance, spins, best_known: int | None = None):
-    s = _spin_array(instance, spins)
-    cut, en = cut_energy_batch(instance, pack_spins(s)[None, :])
-    c, e = int(cut[0].item()), int(en[0].item())
-    q = solution_quality(c, best_known) if best_known is not None else None
-    return EvaluationReport(instance=instance.name, n=instance.n, cut=c, energy=e, quality=q)

@@ -87,7 +87,7 @@ def _result_row(res, n):
 
 
 def gen_fast():
-    rng_kat = {}
+    rng_kat = {"numpy_version": np.__version__}  # the stream below is numpy's (third-party)
     # mix_seed known answers (campaign.py:39-53; KAT at test_campaign.py:44-50)
     rng_kat["mix_seed"] = [
         [m, i, mix_seed(m, i)]

@@ -234,3 +234,25 @@ def test_shard_arithmetic():
     k1, k2 = best_key(100, 5), best_key(100, 3)
     assert k2 > k1 and best_key(101, 9) > k2 and best_key(-5, 0) < best_key(-4, 7)
     assert decode_key(best_key(-17, 42)) == (-17, 42)
+
+
+def test_parse_gset_fast_path_equals_the_references_parser():
+    """parse_gset (one numpy conversion; token loop only for diagnostics) gives
+    the reference's instances and the reference's error messages
+    (instances.py:117-158)."""
+    import importlib
+
+    _reference_campaign()
+    ref = importlib.import_module("gsetbench.instances")
+    good = ["3 2\n1 2 5\n3 2 -1\n", "# c\n4 3 1 2 1\n2 3 -1 # x\n\n3 4 7\n", "1 0", "2 1\n2 1 -3"]
+    for text in good:
+        a, b = parse_gset(text, name="g"), ref.parse_gset(text, name="g")
+        assert (a.n, a.m, a.edges, a.name) == (b.n, b.m, tuple(b.edges), b.name)
+    bad = ["", "3", "0 0", "3 -1", "3 2\n1 2 5\n", "3 1\n1 2 x\n", "3 1\n1 2 3 4\n", "a 1",
+           "3 1\n1 1 2\n", "3 1\n1 9 2\n", "3 2\n1 2 1\n2 1 1\n", "2 1\n1 2 1.5\n"]
+    for text in bad:
+        with pytest.raises(ValueError) as e_ref:
+            ref.parse_gset(text)
+        with pytest.raises(GsetFormatError) as e_ours:
+            parse_gset(text)
+        assert str(e_ours.value) == str(e_ref.value), text

@@ -28,6 +28,18 @@ def test_seedsequence_pcg64_init(oracle):
         assert (hex(s), hex(inc)) == (st["state"], st["inc"]), seed
 
 
+def test_goldens_were_recorded_with_this_numpy():
+    """The PCG64 goldens pin numpy's stream (third-party; the reference only
+    asks for numpy>=1.24, pkg/pyproject.toml:10).  They were recorded with the
+    numpy version stored in the fixture; a different numpy here would mean the
+    reference itself may draw a different stream, so say so loudly."""
+    rec = golden("rng_kat.json")
+    assert rec.get("numpy_version"), "rng_kat.json must record the numpy version it came from"
+    assert np.__version__ == rec["numpy_version"], (
+        f"goldens recorded with numpy {rec['numpy_version']}, running {np.__version__}: "
+        "regenerate tests/golden with tests/golden/make_golden.py and re-pin")
+
+
 def test_pcg64_stream_consumption(oracle):
     for rec in golden("rng_kat.json")["streams"]:
         g = oracle.Pcg64(rec["seed"])
@@ -210,6 +222,85 @@ def test_checker_oracle_statistically_matches_reference(oracle):
                                          3.0, 0.05, spins=False)
     assert int((bc >= 10).sum()) >= 80
     assert int(bc.max()) == 10
+
+
+def _checker_twin(oracle, R, C, w, annealing, S, seed, t0, t1):
+    """Pure-Python restatement of the checkerboard contract (DESIGN.md
+    "Checkerboard contract"; the executable form is
+    oracle/gsb_oracle.c:trial_checker): solvers.py:91-140 line by line with
+    the sweep order (colour 0 in increasing id, then colour 1) and the Philox
+    draws of the contract."""
+    import math
+
+    w = [int(x) for x in w]
+    n, H = R * C, C // 2
+    WPR = (H + 31) // 32
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+
+    def where(v):  # colour, contract word, bit
+        r, c = divmod(v, C)
+        k = c >> 1
+        return (r + c) & 1, r * WPR + (k >> 5), k & 31
+
+    def uniform(p, wi, b, t):
+        u = 0
+        for j in range(8):  # bits 31..24: bit b of plane j
+            u |= ((oracle.philox([wi, t, 2 * p + (j >> 2), 1], key)[j & 3] >> b) & 1) << (31 - j)
+        return u | (oracle.philox([wi, t, 4 + 8 * p + (b >> 2), 1], key)[b & 3] >> 8)
+
+    nb = []
+    for v in range(n):
+        r, c = divmod(v, C)
+        nb.append((((r - 1) % R) * C + c, ((r + 1) % R) * C + c, r * C + (c - 1) % C,
+                   r * C + (c + 1) % C))
+
+    def cut(sp):
+        return sum(w[2 * v] * (sp[v] != sp[nb[v][3]]) + w[2 * v + 1] * (sp[v] != sp[nb[v][1]])
+                   for v in range(n))
+
+    sp = []
+    for v in range(n):
+        p, wi, b = where(v)
+        sp.append(1 if (oracle.philox([wi, 0, p, 0], key)[0] >> b) & 1 else -1)   # solvers.py:96
+    cur = best = cut(sp)                                                          # :101-103
+    bsp, executed = list(sp), 0
+    order = [v for v in range(n) if where(v)[0] == 0] + [v for v in range(n) if where(v)[0] == 1]
+    for t in range(S):                                                            # :107
+        T = (t0 if S == 1 else t0 * (t1 / t0) ** (t / (S - 1))) if annealing else None
+        flipped = False
+        for v in order:                                                           # :111-127
+            up, dn, lf, rt = nb[v]
+            d = sp[v] * (w[2 * v] * sp[rt] + w[2 * v + 1] * sp[dn] + w[2 * lf] * sp[lf] +
+                         w[2 * up + 1] * sp[up])
+            if annealing:
+                acc = d >= 0 or uniform(*where(v), t) < math.ceil(math.exp(d / T) * 2.0**32)
+            else:
+                acc = d > 0
+            if acc:
+                sp[v], cur, flipped = -sp[v], cur + d, True
+                if cur > best:
+                    best, bsp = cur, list(sp)
+        executed = t + 1
+        if not annealing and not flipped:
+            break
+    return best, bsp, executed
+
+
+def test_checker_oracle_matches_python_restatement(oracle):
+    """The C oracle of the checkerboard contract equals the pure-Python
+    restatement (best cut, best spins, sweeps executed) on small even tori,
+    both kinds, including one wider than a 32-site colour word."""
+    from paper_2505_18508_b200.campaign import mix_seeds
+
+    for (R, C, s) in [(4, 4, 1), (4, 6, 2), (6, 10, 3), (4, 70, 4)]:
+        w = oracle.torus_weights(R, C, s)
+        for seed in [int(x) for x in mix_seeds(7, range(2))] + [2**64 - 1]:
+            for kind, S, t0, t1 in [("simulated_annealing_checkerboard", 6, 3.0, 0.05),
+                                    ("simulated_annealing_checkerboard", 4, 0.7, 0.2),
+                                    ("greedy_checkerboard", 20, 0.0, 0.0)]:
+                want = _checker_twin(oracle, R, C, w, kind.startswith("sim"), S, seed, t0, t1)
+                bc, bs, se = oracle.run_trials_checker(R, C, w, kind, S, [seed], t0, t1)
+                assert (int(bc[0]), [int(x) for x in bs[0]], int(se[0])) == want, (R, C, seed, kind)
 
 
 def test_random_scan_contract_agrees_in_law_with_reference(oracle):
