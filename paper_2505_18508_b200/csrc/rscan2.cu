@@ -110,12 +110,12 @@ void rscan2_test_limits(int tqcap, int lcap) {
 }
 
 // Team shape for T trials.  Cost model (arbitrary units, fitted to B200 runs
-// of configs 1-4): a wave of k resident trials per SM takes
-//   RB * max(k * NW / 8, 1) * (1 + 0.05 log2 NW)
-// -- issue-bound once ~8 warps per SM are busy, latency-bound below (then
-// more warps per trial help), a small barrier cost per extra warp -- summed
-// over the waves the occupancy allows.  `occupancy` false (no device): only
-// feasibility, first fit.
+// of configs 1-4): with w = k * NW warps resident per SM the SM's throughput
+// saturates like w / (w + 12), so a wave of k resident trials per SM takes
+//   RB * (k * NW + 12) * (1 + 0.03 log2 NW)
+// (work k * NW * RB over that throughput; a small barrier cost per extra
+// warp), summed over the waves the occupancy allows.  `occupancy` false (no
+// device): only feasibility, first fit.
 static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupancy, Rs2Shape &sh) {
   const int WPR = (cols + 31) / 32;
   if (WPR > 32) return false;
@@ -136,11 +136,8 @@ static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupanc
       if (per_sm < 1) continue;
       const long long tps = ((long long)T + nsm - 1) / nsm;  // trials per SM
       const long long full = tps / per_sm, rem = tps % per_sm;
-      const double bar = 1.0 + 0.05 * (nw == 1 ? 0 : nw == 2 ? 1 : nw == 4 ? 2 : 3);
-      auto wave = [&](long long k) {
-        const double load = (double)k * nw / 8.0;
-        return (double)RB * (load > 1.0 ? load : 1.0) * bar;
-      };
+      const double bar = 1.0 + 0.03 * (nw == 1 ? 0 : nw == 2 ? 1 : nw == 4 ? 2 : 3);
+      auto wave = [&](long long k) { return (double)RB * ((double)k * nw + 12.0) * bar; };
       const double cost = (double)full * wave(per_sm) + (rem ? wave(rem) : 0.0);
       if (!found || cost < bestcost - 1e-9) {
         found = true;

@@ -251,9 +251,11 @@ __device__ __forceinline__ void rs2_tie_resolve(uint2 it, const Rs2Tie &c, uint3
 }
 
 // register cap: 14 resident warps per SM (144 registers) for teams of 1-2
-// warps, 16 (128) for larger teams unless 7 rows per lane need more
+// warps, 16 (128) for larger teams unless 7 rows per lane need more; 8 warps
+// x 2 rows run 24 warps per SM at 80 registers (config 2: +10 % over 4 x 4 at
+// 128; lower caps for the other shapes only spill, profiles/r02_rscan2_regcaps.txt)
 constexpr int rs2_max_regs(int NW, int RB) {
-  return NW <= 2 ? 144 : NW == 4 ? (RB >= 7 ? 168 : 128) : (RB >= 7 ? 255 : 128);
+  return NW <= 2 ? 144 : NW == 4 ? (RB >= 7 ? 168 : 128) : (RB >= 7 ? 255 : RB == 2 ? 80 : 128);
 }
 
 template <int NW, int RB, bool SA>
@@ -411,12 +413,8 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
         K2f = a.table[(size_t)t * 4 + 1];
         K4f = a.table[(size_t)t * 4 + 3];
       }
-      uint32_t kb2[8], kb4[8];
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        kb2[i] = (uint32_t)((int32_t)((uint32_t)K2f << i) >> 31);
-        kb4[i] = (uint32_t)((int32_t)((uint32_t)K4f << i) >> 31);
-      }
+      // thresholds' top bytes at bits 31..24 (plane i of K = bit 31 - i)
+      const uint32_t K2w = (uint32_t)K2f, K4w = (uint32_t)K4f;
       const uint32_t all2 = K2f > 0xFFFFFFFFull ? ~0u : 0u, all4 = K4f > 0xFFFFFFFFull ? ~0u : 0u;
       uint32_t fixmask = 0;  // slots whose fix-up word is in use
       auto push_tie = [&](int j, uint32_t item_a, uint32_t kind_flags) {
@@ -453,8 +451,8 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
           uint32_t lt2 = 0, ne2 = 0, lt4 = 0, ne4 = 0;
 #pragma unroll
           for (int i = 7; i >= 0; i--) {
-            cmp_step(up8[i], kb2[i], lt2, ne2);
-            cmp_step(up8[i], kb4[i], lt4, ne4);
+            cmp_step(up8[i], (uint32_t)((int32_t)(K2w << i) >> 31), lt2, ne2);
+            cmp_step(up8[i], (uint32_t)((int32_t)(K4w << i) >> 31), lt4, ne4);
           }
           const uint32_t vs = vslot(j);
           const uint32_t t2 = ~ne2 & vs & ~all2, t4 = ~ne4 & vs & ~all4;
