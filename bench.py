@@ -532,6 +532,14 @@ def main(argv=None):
     pe1.record(stream)
     torch.cuda.synchronize()
     philox_peak = nthr * bpt / (pe0.elapsed_time(pe1) / 1e3)  # blocks/s
+    lpt = 1 << 17
+    _lib.check(L.gsb_lop3_bench(1024, sink.data_ptr(), sp))
+    torch.cuda.synchronize()
+    pe0.record(stream)
+    _lib.check(L.gsb_lop3_bench(lpt, sink.data_ptr(), sp))
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    lop3_peak = nthr * lpt / (pe0.elapsed_time(pe1) / 1e3)  # LOP3 (thread ops)/s
 
     # ---- roofline of the dominant kernel (the sweep kernel of this torus)
     if is_rscan:
@@ -558,6 +566,40 @@ def main(argv=None):
                           "no measured SMEM peak in MEASURED_PEAKS.json)"}
     if blocks_per_step is not None:
         rng_achieved = blocks_per_step / launch_s
+        philox_roof = {
+            "unit": "Gblock/s (Philox4x32-10)", "achieved": rng_achieved / 1e9,
+            "peak": philox_peak / 1e9, "frac": rng_achieved / philox_peak,
+            "algorithmic_units_per_launch": blocks_per_step, "unit_def": unit_def,
+            "peak_basis": "measured live: gsb_philox_bench, SMs x 8 x 256 threads, 2 independent "
+                          "Philox4x32-10 blocks in flight per thread, CUDA events"}
+    if is_rscan:
+        # ALU-pipe (LOP3/SHF) operations the contract's bit-sliced algorithm needs per
+        # 32-site word and sweep:
+        #   Philox XOR halves 4 blocks x 16, acceptance compare 8 planes x 2 thresholds x 2,
+        #   precedence 2 directions x 8 planes x 2 + 8 plane alignments x 2 + 2,
+        #   Delta of the flips 30; per round (ready set, Delta classes, accept, commit) 25
+        fixed, per_round = (64 + 32 + 50 + 30, 25) if cfg.annealing else (32 + 50 + 30, 22)
+        words = rows * ((cols + 31) // 32)
+        sweeps_run = int(sweeps_d.sum().item())
+        alu_ops = words * (fixed * sweeps_run + per_round * rs_stats["rounds_per_sweep"] * sweeps_run)
+        roofline = {
+            "bound": "int", "unit": "Tops/s (ALU-pipe integer thread operations: LOP3/SHF)",
+            "achieved": alu_ops / launch_s / 1e12, "peak": lop3_peak / 1e12,
+            "frac": alu_ops / launch_s / lop3_peak, "traffic": None,
+            "kernel": sweep_kernel,
+            "algorithmic_units_per_launch": alu_ops,
+            "unit_def": f"{fixed} + {per_round} x rounds ALU-pipe operations per 32-site word and "
+                        "sweep: what the contract's level-synchronous bit-sliced algorithm needs "
+                        "(Philox XORs, 8-plane comparators, ready sets, Delta classes, commit); "
+                        "rounds per sweep counted by the kernel; the kernel's own overheads "
+                        "(shuffles, ties, best-so-far, barriers) are not counted",
+            "peak_basis": "measured live: gsb_lop3_bench, SMs x 8 x 256 threads, 8 independent "
+                          "LOP3 chains per thread, CUDA events (the ALU pipe issues one warp "
+                          "instruction per 2 cycles per SM sub-partition)",
+            "updates_per_launch": upd_rank, "launch_ms": launch_s * 1e3,
+            "updates_per_s": kernel_rate, "philox": philox_roof, "smem": smem,
+        }
+    elif blocks_per_step is not None:
         roofline = {
             "bound": "int", "unit": "Gblock/s (Philox4x32-10)",
             "achieved": rng_achieved / 1e9, "peak": philox_peak / 1e9,

@@ -167,6 +167,11 @@ int gsb_workspace_counters(const void *workspace_dev, void *stream, uint64_t *ph
  * SMs x 8 x 256 threads, each evaluating blocks_per_thread blocks. */
 int gsb_philox_bench(int64_t blocks_per_thread, uint32_t *sink_dev, void *stream);
 
+/* ALU-pipe throughput probe (roofline denominator of the bit-sliced kernels):
+ * SMs x 8 x 256 threads, each issuing lop3_per_thread LOP3 (8 independent
+ * chains; a multiple of 32). */
+int gsb_lop3_bench(int64_t lop3_per_thread, uint32_t *sink_dev, void *stream);
+
 /* reference engine on a general graph (any integer weights, dmax = max_i sum_j |w_ij|) */
 size_t gsb_graph_workspace_bytes(const gsb_graph *g, int32_t sweeps, int32_t T);
 int gsb_graph_sweep(const gsb_graph *g, int kind, int32_t sweeps, const uint64_t *table_dev,

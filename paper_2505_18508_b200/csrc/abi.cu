@@ -299,6 +299,11 @@ int gsb_philox_bench(int64_t blocks_per_thread, uint32_t *sink_dev, void *stream
   return philox_bench(blocks_per_thread, sink_dev, (cudaStream_t)stream);
 }
 
+int gsb_lop3_bench(int64_t lop3_per_thread, uint32_t *sink_dev, void *stream) {
+  if (lop3_per_thread < 32 || !sink_dev) return set_error(GSB_EINVAL, "bad arguments");
+  return lop3_bench(lop3_per_thread, sink_dev, (cudaStream_t)stream);
+}
+
 int gsb_workspace_status(const void *ws, void *stream) {
   if (!ws) return set_error(GSB_EINVAL, "null workspace");
   return finish_check((int *)ws, (cudaStream_t)stream);

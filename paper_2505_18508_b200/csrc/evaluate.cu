@@ -168,6 +168,40 @@ __global__ void __launch_bounds__(256) philox_bench_kernel(int64_t n, uint32_t *
 
 int philox_bench_threads() { return num_sms() * 8 * 256; }
 
+// ALU-pipe probe: 8 independent LOP3 chains per thread (3-input boolean
+// functions, the instruction the bit-sliced sweep kernels are made of);
+// n = LOP3 per thread.  SMs x 8 x 256 threads, as the Philox probe.
+__global__ void __launch_bounds__(256) lop3_bench_kernel(int64_t n, uint32_t *sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t a0 = tid, a1 = tid * 3u + 1u, a2 = tid ^ 0x5bd1e995u, a3 = ~tid, a4 = tid + 77u,
+           a5 = tid * 7u, a6 = tid ^ 0xdeadbeefu, a7 = tid - 13u;
+  const uint32_t m = 0x9e3779b9u ^ blockIdx.x, k = 0x85ebca6bu + threadIdx.x;
+  const int iters = (int)(n / 32);
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a0) : "r"(m), "r"(a1));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0xE8;" : "+r"(a1) : "r"(k), "r"(a2));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x69;" : "+r"(a2) : "r"(m), "r"(a3));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0xCA;" : "+r"(a3) : "r"(k), "r"(a4));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x8E;" : "+r"(a4) : "r"(m), "r"(a5));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0xBE;" : "+r"(a5) : "r"(k), "r"(a6));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0xB4;" : "+r"(a6) : "r"(m), "r"(a7));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0xD8;" : "+r"(a7) : "r"(k), "r"(a0));
+    }
+  }
+  const uint32_t acc = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7;
+  if (acc == 0x8badf00du) sink[tid & 255] = acc;  // keep the work alive
+}
+
+int lop3_bench(int64_t lop3_per_thread, uint32_t *sink, cudaStream_t stream) {
+  const int nsm = num_sms();
+  if (nsm <= 0) return set_error(GSB_ECUDA, "no CUDA device");
+  lop3_bench_kernel<<<nsm * 8, 256, 0, stream>>>(lop3_per_thread, sink);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GSB_OK : set_error(GSB_ECUDA, cudaGetErrorString(e));
+}
+
 int philox_bench(int64_t blocks_per_thread, uint32_t *sink, cudaStream_t stream) {
   const int nsm = num_sms();
   if (nsm <= 0) return set_error(GSB_ECUDA, "no CUDA device");

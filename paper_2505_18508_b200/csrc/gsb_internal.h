@@ -77,6 +77,7 @@ int torus_weights(int rows, int cols, uint64_t seed, int8_t *w, cudaStream_t str
 int best_key(const int64_t *best_cut, int T, int64_t first, int64_t *key, cudaStream_t stream);
 int philox_bench(int64_t blocks_per_thread, uint32_t *sink, cudaStream_t stream);
 int philox_bench_threads();
+int lop3_bench(int64_t lop3_per_thread, uint32_t *sink, cudaStream_t stream);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -216,3 +216,40 @@ def test_run_trials_device_on_a_side_stream():
         side.synchronize()
         for o in outs:
             assert torch.equal(o[0], ref[0]) and torch.equal(o[2], ref[2])
+
+
+def test_integration_ctypes_stub():
+    """INTEGRATION.md's `gsetbench/_b200.py` stub, taken verbatim from the
+    markdown and executed: the bit-exact engine through it reproduces the
+    reference's own config-1 trajectories (goldens), and the random-scan engine
+    through it equals the package's result."""
+    import os
+    import re
+    import types
+
+    from conftest import ROOT
+    from paper_2505_18508_b200 import _lib
+    from paper_2505_18508_b200.solvers import ANNEALING_RANDOM_SCAN
+
+    md = (ROOT / "INTEGRATION.md").read_text()
+    code = re.search(r"```python\n(# gsetbench/_b200\.py.*?)```", md, re.S).group(1)
+    os.environ["GSB_LIB"] = str(_lib.LIB_PATH)
+    stub = types.ModuleType("gsetbench_b200_stub")
+    exec(compile(code, "INTEGRATION.md:_b200.py", "exec"), stub.__dict__)
+    c1 = golden("c1_full.json")
+    rows = c1["runs"]["simulated_annealing"]["trials"][:6]
+    spec = TorusSpec(c1["rows"], c1["cols"], 1)
+    best, done, bits = stub.run_trials_torus(spec, "simulated_annealing", c1["sweeps"],
+                                             [r["seed"] for r in rows], 3.0, 0.05, engine=0)
+    n = spec.rows * spec.cols
+    for i, r in enumerate(rows):
+        assert (int(best[i]), int(done[i]), bits[i].tobytes().hex()[:(n + 3) // 4]) == (
+            r["best_cut"], r["sweeps_executed"], r["hex"])
+    seeds = [r["seed"] for r in rows]
+    b2, d2, bits2 = stub.run_trials_torus(spec, ANNEALING_RANDOM_SCAN, 50, seeds, 3.0, 0.05,
+                                          engine=4)
+    ours = run_trials(generate_torus(spec), default_config(ANNEALING_RANDOM_SCAN, 50, 0), seeds)
+    assert np.array_equal(b2, ours.best_cut) and np.array_equal(bits2, ours.bits)
+    with pytest.raises(ValueError):
+        stub.run_trials_torus(TorusSpec(5, 5, 1), "simulated_annealing_checkerboard", 5, [1],
+                              3.0, 0.05, engine=1)  # odd torus: GSB_EUNSUPPORTED -> ValueError
