@@ -1,8 +1,8 @@
 // rscan2.cu -- random-scan engine (kinds *_random_scan): host side.
 //
 // Team shape selection and launch of rscan2_kernel<NW, RB, SA>
-// (rscan2_kernel.cuh has the algorithm; rscan2_nw{1,2,4,8}.cu the
-// instantiations).  NW warps per trial in {1, 2, 4, 8}, RB rows per lane in
+// (rscan2_kernel.cuh has the algorithm; rscan2_nw{1,2,4,7,8}.cu the
+// instantiations).  NW warps per trial in {1, 2, 4, 7, 8}, RB rows per lane in
 // {1, 2, 3, 4, 5, 7}: a torus fits when rows <= NW * floor(32 / WPR) * RB for
 // some shape, WPR = ceil(cols / 32) <= 32.
 #include <cuda_runtime.h>
@@ -18,7 +18,7 @@ struct Rs2Shape {
 };
 
 static const int kRbSet[] = {1, 2, 3, 4, 5, 7};
-static const int kNwSet[] = {1, 2, 4, 8};
+static const int kNwSet[] = {1, 2, 4, 7, 8};
 
 static const void *rs2_kernel(int nw, int rb, bool sa) {
   switch (nw) {
@@ -28,6 +28,8 @@ static const void *rs2_kernel(int nw, int rb, bool sa) {
       return rs2_kernel_nw2(rb, sa);
     case 4:
       return rs2_kernel_nw4(rb, sa);
+    case 7:
+      return rs2_kernel_nw7(rb, sa);
     case 8:
       return rs2_kernel_nw8(rb, sa);
     default:
@@ -136,7 +138,7 @@ static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupanc
       if (per_sm < 1) continue;
       const long long tps = ((long long)T + nsm - 1) / nsm;  // trials per SM
       const long long full = tps / per_sm, rem = tps % per_sm;
-      const double bar = 1.0 + 0.03 * (nw == 1 ? 0 : nw == 2 ? 1 : nw == 4 ? 2 : 3);
+      const double bar = 1.0 + 0.03 * (nw == 1 ? 0 : nw == 2 ? 1 : nw == 4 ? 2 : 3);  // ~log2 NW
       auto wave = [&](long long k) { return (double)RB * ((double)k * nw + 12.0) * bar; };
       const double cost = (double)full * wave(per_sm) + (rem ? wave(rem) : 0.0);
       if (!found || cost < bestcost - 1e-9) {

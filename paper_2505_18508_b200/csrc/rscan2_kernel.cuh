@@ -1,6 +1,6 @@
 // rscan2_kernel.cuh -- random-scan engine (kinds *_random_scan), contract v2:
 // the kernel template.  Host side and shape selection: rscan2.cu; the
-// instantiations are spread over rscan2_nw{1,2,4,8}.cu to compile in parallel.
+// instantiations are spread over rscan2_nw{1,2,4,7,8}.cu to compile in parallel.
 //
 // The reference sweep (solvers.py:107-127) visits every site once in a fresh
 // uniformly random order and updates it from its current neighbours.  Here
@@ -63,6 +63,9 @@
 
 namespace gsb {
 
+#ifndef RS2_RPB
+#define RS2_RPB 1  // rounds between team barriers (step 3); 2-6 measured equal or slower
+#endif
 constexpr uint32_t RS2_TAG = 5u;
 constexpr int RS2_CAP = 256;  // events sorted at once in step 4b
 
@@ -167,6 +170,38 @@ __device__ __forceinline__ void cmp8(const uint32_t *x, const uint32_t *y, uint3
   tie = ~ne;
 }
 
+// ---- TMA bulk copy global -> shared, completion on an mbarrier (prologue:
+// the instance's couplings are staged once per CTA)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void tma_bulk_load(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                              unsigned long long *mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(mbar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}" ::"r"(smem_u32(mbar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int NW>
 __device__ __forceinline__ void team_sync() {
   if (NW == 1)
@@ -255,7 +290,9 @@ __device__ __forceinline__ void rs2_tie_resolve(uint2 it, const Rs2Tie &c, uint3
 // x 2 rows run 24 warps per SM at 80 registers (config 2: +10 % over 4 x 4 at
 // 128; lower caps for the other shapes only spill, profiles/r02_rscan2_regcaps.txt)
 constexpr int rs2_max_regs(int NW, int RB) {
-  return NW <= 2 ? 144 : NW == 4 ? (RB >= 7 ? 168 : 128) : (RB >= 7 ? 255 : RB == 2 ? 80 : 128);
+  return NW <= 2 ? 144
+                 : NW == 4 ? (RB >= 7 ? 168 : 128)
+                           : (RB >= 7 ? 255 : RB == 2 ? 80 : 128);  // 7 or 8 warps
 }
 
 template <int NW, int RB, bool SA>
@@ -313,7 +350,23 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
   auto vslot = [&](int j) -> uint32_t { return j == RB - 1 ? Vlast : V; };
   auto row_of = [&](int j) { return start + (j < nr ? j : 0); };
 
-  // ---- couplings (instance constants): bit b of N* = weight of that edge < 0
+  // ---- couplings (instance constants): bit b of N* = weight of that edge < 0.
+  // The int8 array w[2n] is staged in shared memory by one TMA bulk copy when
+  // it fits the plane / event regions (free before the first trial) and its
+  // size is a multiple of 16 bytes; else the planes are read from global memory.
+  __shared__ __align__(8) unsigned long long s_mbar;
+  const int8_t *wsrc = a.w;
+  {
+    const uint32_t wbytes = 2u * (uint32_t)a.n;
+    if (wbytes % 16u == 0u && wbytes <= (uint32_t)(48 * RB * NT) &&
+        ((uintptr_t)a.w & 15u) == 0) {  // team-uniform
+      if (tid == 0) mbar_init(&s_mbar, 1);
+      team_sync<NW>();
+      if (tid == 0) tma_bulk_load(smem_raw, a.w, wbytes, &s_mbar);
+      mbar_wait(&s_mbar, 0);
+      wsrc = (const int8_t *)smem_raw;
+    }
+  }
   uint32_t Nr[RB], Nl[RB], Nd[RB], Nu0 = 0;
 #pragma unroll
   for (int j = 0; j < RB; j++) {
@@ -323,9 +376,9 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
       for (int b = 0; b < vb; b++) {
         const int col = col0 + b, v = r * cols + col;
         const int vl = r * cols + (col == 0 ? cols - 1 : col - 1);
-        nrr |= (uint32_t)(a.w[2 * v] < 0) << b;
-        ndd |= (uint32_t)(a.w[2 * v + 1] < 0) << b;
-        nll |= (uint32_t)(a.w[2 * vl] < 0) << b;
+        nrr |= (uint32_t)(wsrc[2 * v] < 0) << b;
+        ndd |= (uint32_t)(wsrc[2 * v + 1] < 0) << b;
+        nll |= (uint32_t)(wsrc[2 * vl] < 0) << b;
       }
     }
     Nr[j] = nrr;
@@ -334,10 +387,12 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
   }
   if (act) {
     const int ru = start == 0 ? rows - 1 : start - 1;
-    for (int b = 0; b < vb; b++) Nu0 |= (uint32_t)(a.w[2 * (ru * cols + col0 + b) + 1] < 0) << b;
+    for (int b = 0; b < vb; b++) Nu0 |= (uint32_t)(wsrc[2 * (ru * cols + col0 + b) + 1] < 0) << b;
   }
 
-  unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
+    team_sync<NW>();  // the staged couplings are consumed: the regions are free
+
+unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
 #ifdef GSB_RS2_PROF
   long long pf[6] = {0, 0, 0, 0, 0, 0}, pf_t = clock64();
 #define RS2_TICK(i)                   \
@@ -553,15 +608,26 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
       const uint32_t Pu0 = ~s_xpd[tid_above];
       RS2_TICK(1);
 
-      // ---- 3. rounds
+      // ---- 3. rounds.  The edge rows (S, U) are exchanged through one 64-bit
+      // word per lane, written after every round and read without waiting for
+      // the other warps: a stale value only shows a neighbour as still
+      // unvisited (the site then waits a round), and a site seen as visited
+      // has its final spin in the same word.  The team meets at a barrier only
+      // every RS2_RPB rounds (end-of-sweep test); lanes of one warp exchange
+      // in step (syncwarp).  (One buffer instead of two per round: +2.5 %.
+      // Fewer barriers gain nothing: the sweep then ends at a multiple of
+      // RS2_RPB rounds, profiles/r02_rscan2_rounds_per_barrier.txt.)
+      volatile unsigned long long *const xt = (volatile unsigned long long *)(s_xtop + par * NT);
+      volatile unsigned long long *const xb = (volatile unsigned long long *)(s_xbot + par * NT);
       for (int rr = 0;; rr++) {
         if (rr >= 1 << 16) {
           if (tid == 0) atomicExch(a.err, GSB_EUNSUPPORTED);
           break;
         }
         st_rounds++;
-        const uint2 xu = s_xbot[par * NT + tid_above];  // (S, U) of the row above slot 0
-        const uint2 xd = s_xtop[par * NT + tid_below];  // (S, U) of the row below the last
+        const unsigned long long xu64 = xb[tid_above], xd64 = xt[tid_below];
+        const uint2 xu = make_uint2((uint32_t)xu64, (uint32_t)(xu64 >> 32));  // row above slot 0
+        const uint2 xd = make_uint2((uint32_t)xd64, (uint32_t)(xd64 >> 32));  // row below the last
         uint32_t left = 0;
 #pragma unroll
         for (int j = 0; j < RB; j++) {
@@ -610,11 +676,15 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
           U[j] = u ^ ready;
           left |= U[j];
         }
-        par ^= 1;
-        s_xtop[par * NT + tid] = make_uint2(S[0], U[0]);
-        s_xbot[par * NT + tid] = make_uint2(last_of(S), last_of(U));
-        if (!team_any<NW>(left != 0)) break;
+        xt[tid] = (unsigned long long)S[0] | ((unsigned long long)U[0] << 32);
+        xb[tid] = (unsigned long long)last_of(S) | ((unsigned long long)last_of(U) << 32);
+        if (rr % RS2_RPB == RS2_RPB - 1) {
+          if (!team_any<NW>(left != 0)) break;
+        } else {
+          __syncwarp();
+        }
       }
+      par ^= 1;
 
       RS2_TICK(2);
       // ---- 4. Delta of every flip at its visit, sums, best-so-far
@@ -1052,6 +1122,7 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
 const void *rs2_kernel_nw1(int rb, bool sa);
 const void *rs2_kernel_nw2(int rb, bool sa);
 const void *rs2_kernel_nw4(int rb, bool sa);
+const void *rs2_kernel_nw7(int rb, bool sa);
 const void *rs2_kernel_nw8(int rb, bool sa);
 
 #define RS2_DEFINE_TABLE(NWV)                                                   \
