@@ -198,6 +198,10 @@ int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.lcap = RS2_CAP;
   if (g_test_tqcap > 0 && g_test_tqcap < a.tqcap) a.tqcap = g_test_tqcap;  // smem sized for the default
   if (g_test_lcap > 0) a.lcap = g_test_lcap;
+  a.m_one = 1u;
+  a.m_two = 2u;
+  a.m_neg = 0xFFFFFFFFu;
+  a.m_last = 1u << (a.lastvalid - 1);
   a.err = err_ws;
   a.stats = stats;
   const size_t smem = rs2_smem_bytes(sh.NW, sh.RB, rs2_tqcap(a.n), a.nstream);

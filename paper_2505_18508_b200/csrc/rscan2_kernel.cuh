@@ -83,6 +83,10 @@ struct Rs2Args {
   int nbytes, nstream;  // output bytes per trial, 32-bit words of the staged bitstring
   int tqcap;            // tie queue capacity (items)
   int lcap;             // events sorted at once in step 4b (<= RS2_CAP; smaller in tests)
+  // multipliers the compiler cannot fold (1, 2, 0xFFFFFFFF, 1 << (lastvalid - 1)): the
+  // rounds are bound by the ALU pipe, so additions of disjoint bit sets and
+  // shifts by these are written as multiply-adds, which issue on the FMA pipe
+  uint32_t m_one, m_two, m_neg, m_last;
   int *err;
   // [0] rounds, [1] gated sweeps, [2] candidate buckets, [3] ties (queued or inline),
   // [4..9] cycles per phase (GSB_RS2_PROF builds)
@@ -139,7 +143,8 @@ __device__ __forceinline__ uint32_t rs2_low24(uint32_t wi, uint32_t t, uint32_t 
 }
 
 // top byte (planes 0..7, plane 0 = MSB) of bit b: each plane's bit is moved to
-// bit 31 and funnel-shifted into the key (2 SHF per plane)
+// bit 31 and funnel-shifted into the key (2 SHF per plane).  (As multiply-adds
+// on the FMA pipe -- 3 per plane, one dependent chain -- it measured 3 % slower.)
 __device__ __forceinline__ uint32_t gather8(const uint4 &a, const uint4 &b, int bit) {
   const int sh = 31 - bit;
   uint32_t r = 0;
@@ -335,7 +340,7 @@ __global__ void __maxnreg__(rs2_max_regs(NW, RB)) rscan2_kernel(Rs2Args a) {
   const uint32_t V = act ? (vb == 32 ? 0xFFFFFFFFu : (1u << vb) - 1u) : 0u;
   const uint32_t Vlast = shortb ? 0u : V;
   const int cpos = vb - 1;
-  const uint32_t Mr = 1u << cpos;
+  const uint32_t Mr = c == WPR - 1 ? a.m_last : 0x80000000u;  // 1 << cpos, opaque (see m_last)
   const int ppos = (c == 0 ? a.lastvalid : 32) - 1;
   const int rsrc = act ? rbl * WPR + (c + 1 == WPR ? 0 : c + 1) : lane;
   const int lsrc = act ? rbl * WPR + (c == 0 ? WPR - 1 : c - 1) : lane;
@@ -646,10 +651,11 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
           }
           const uint32_t rS = __shfl_sync(0xffffffffu, s, rsrc);
           const uint32_t rU = __shfl_sync(0xffffffffu, u, rsrc);
-          const uint32_t lS = __shfl_sync(0xffffffffu, s, lsrc);
-          const uint32_t lU = __shfl_sync(0xffffffffu, u, lsrc);
-          const uint32_t RS = (s >> 1) + rS * Mr, RU = (u >> 1) + rU * Mr;
-          const uint32_t LS = s * 2u + (lS >> ppos), LU = u * 2u + (lU >> ppos);
+          // the left neighbour sends its last valid bit at bit 0 (its cpos = our ppos)
+          const uint32_t lS = __shfl_sync(0xffffffffu, s >> cpos, lsrc);
+          const uint32_t lU = __shfl_sync(0xffffffffu, u >> cpos, lsrc);
+          const uint32_t RS = rS * Mr + (s >> 1), RU = rU * Mr + (u >> 1);
+          const uint32_t LS = s * a.m_two + lS, LU = u * a.m_two + lU;
           uint32_t blk = Pr[j] & RU;
           blk = lop3<0xF8>(blk, Pl[j], LU);  // | (Pl & LU)
           blk = lop3<0xF8>(blk, Pd[j], dnU);
@@ -672,8 +678,8 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
             flip = ready & lop3<0xE0>(c1, s1, td);  // >= 3 positive terms
           }
           S[j] = s ^ flip;
-          F[j] ^= flip;
-          U[j] = u ^ ready;
+          F[j] = flip * a.m_one + F[j];   // disjoint bits: a site flips once per sweep
+          U[j] = ready * a.m_neg + u;     // ready is a subset of u
           left |= U[j];
         }
         xt[tid] = (unsigned long long)S[0] | ((unsigned long long)U[0] << 32);
@@ -713,10 +719,10 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
           }
           const uint32_t rS = __shfl_sync(0xffffffffu, s, rsrc);
           const uint32_t rF = __shfl_sync(0xffffffffu, f, rsrc);
-          const uint32_t lS = __shfl_sync(0xffffffffu, s, lsrc);
-          const uint32_t lF = __shfl_sync(0xffffffffu, f, lsrc);
-          const uint32_t RS = (s >> 1) + rS * Mr, RF = (f >> 1) + rF * Mr;
-          const uint32_t LS = s * 2u + (lS >> ppos), LF = f * 2u + (lF >> ppos);
+          const uint32_t lS = __shfl_sync(0xffffffffu, s >> cpos, lsrc);
+          const uint32_t lF = __shfl_sync(0xffffffffu, f >> cpos, lsrc);
+          const uint32_t RS = rS * Mr + (s >> 1), RF = rF * Mr + (f >> 1);
+          const uint32_t LS = s * a.m_two + lS, LF = f * a.m_two + lF;
           if (!SA) anyf |= f != 0;
           // neighbour spin at the visit: final if it precedes, else initial
           const uint32_t xr = lop3<0xB4>(RS, RF, Pr[j]);  // S ^ (F & ~P)
