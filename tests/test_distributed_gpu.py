@@ -112,3 +112,29 @@ def test_run_campaign_shards_over_the_process_group(tmp_path):
     strip = lambda recs: [(r.index, r.seed, r.best_cut, r.sweeps_executed, r.spins_hex)  # noqa: E731
                           for r in recs]
     assert strip(read_log(log2)) == strip(read_log(log1)) and len(read_log(log2)) == 21
+
+
+@pytest.mark.parametrize("scaling,trials", [("weak", 200), ("strong", 100)])
+def test_bench_gpus_2_on_one_gpu(scaling, trials):
+    """`bench.py --gpus 2` starts its two ranks itself; here both share the one
+    GPU over gloo (GSB_BENCH_SHARE_GPU=1, a development arrangement: plumbing,
+    not a measurement).  The line reports n_gpus 2 and the campaign-wide best."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, GSB_BENCH_SHARE_GPU="1")
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--sweeps", "40",
+         "--steps", "1", "--warmup", "1", "--no-cpu", "--no-secondary", "--scaling", scaling],
+        capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["config"]["trials"] == trials
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 2
+    assert d["config"]["kind"] == "simulated_annealing_random_scan"
