@@ -1,6 +1,7 @@
 // evaluate.cu -- exact cut / energy evaluator (evaluate.py:35-49), torus weight
 // generation (instances.py:203-224) and the multi-GPU best-key helper.
 #include <cstdint>
+#include <cstring>
 
 #include "gsb_device.cuh"
 #include "gsb_internal.h"
@@ -11,32 +12,114 @@ __device__ __forceinline__ int get_bit(const uint8_t *__restrict__ b, int x) {
   return (b[x >> 3] >> (7 - (x & 7))) & 1;
 }
 
-// grid (blocks_per_trial, T); every site contributes its right and down edge
-__global__ void torus_cut_energy_kernel(int rows, int cols, const int8_t *__restrict__ w,
-                                        const uint8_t *__restrict__ bits, int nbytes,
-                                        unsigned long long *cut, unsigned long long *energy) {
-  const int n = rows * cols;
-  const uint8_t *b = bits + (size_t)blockIdx.y * nbytes;
-  long long c = 0, e = 0;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-    int r = x / cols, cc = x - r * cols;
-    int right = r * cols + (cc + 1 == cols ? 0 : cc + 1);
-    int down = (r + 1 == rows ? 0 : r + 1) * cols + cc;
-    int sx = get_bit(b, x), sr = get_bit(b, right), sd = get_bit(b, down);
-    int wr = w[2 * x], wd = w[2 * x + 1];
-    if (sx != sr) c += wr;
-    if (sx != sd) c += wd;
-    e += (sx == sr) ? wr : -wr;
-    e += (sx == sd) ? wd : -wd;
+// 32 stream bits starting at bit `off` of an MSB-first packed bitstring
+// (bit 31 of the result = stream bit off); reads two 32-bit words, the second
+// only if it exists.
+__device__ __forceinline__ uint32_t stream32(const uint8_t *__restrict__ b, int nbytes, int off) {
+  const int W = off >> 5, sh = off & 31;
+  auto be = [&](int w) -> uint32_t {
+    const int o = 4 * w;
+    if (o + 4 <= nbytes) {
+      uint32_t v;
+      memcpy(&v, b + o, 4);  // rows of `bits` are nbytes apart: not always 4-byte aligned
+      return __byte_perm(v, 0u, 0x0123);
+    }
+    uint32_t v = 0;
+    for (int i = 0; i < 4; i++)
+      if (o + i < nbytes) v |= (uint32_t)b[o + i] << (24 - 8 * i);
+    return v;
+  };
+  const uint32_t hi = be(W);
+  return sh ? __funnelshift_l(be(W + 1), hi, sh) : hi;
+}
+
+// K1, the bit-sliced evaluator: one thread per (row, 32-column
+// chunk); the chunk's coupling sign planes are built once and reused for
+// every trial of the slab blockIdx.y covers.  Per trial and chunk: three
+// 32-bit windows of the MSB-first bitstring (the sites, their right and their
+// down neighbours) and four popcounts.  cut = sum over edges with differing
+// spins of w; energy = W - 2 cut (evaluate.py:10-12).  A chunk with a weight
+// other than +-1 takes the per-site path (any int8 weights stay exact).
+__global__ void __launch_bounds__(256)
+    torus_cut_energy_kernel(int rows, int cols, int WPR, const int8_t *__restrict__ w,
+                            const uint8_t *__restrict__ bits, int nbytes, int T, int slab,
+                            unsigned long long *cut, unsigned long long *energy) {
+  __shared__ long long red[8];
+  const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nchunks = rows * WPR;
+  const bool act = chunk < nchunks;
+  const int r = act ? chunk / WPR : 0, k = act ? chunk - r * WPR : 0;
+  const int c0 = 32 * k, vb = act ? min(32, cols - c0) : 0;
+  const uint32_t valid = vb == 0 ? 0u : (vb == 32 ? ~0u : ~0u << (32 - vb));
+  const int rd = r + 1 == rows ? 0 : r + 1;
+  // sign planes, MSB-first like the stream: bit 31 - b = site (r, c0 + b)
+  uint32_t negR = 0, negD = 0;
+  bool unit = true;
+  long long wsum = 0;
+  for (int b = 0; b < vb; b++) {
+    const int x = r * cols + c0 + b;
+    const int wr = w[2 * x], wd = w[2 * x + 1];
+    negR |= (uint32_t)(wr < 0) << (31 - b);
+    negD |= (uint32_t)(wd < 0) << (31 - b);
+    unit = unit && (wr == 1 || wr == -1) && (wd == 1 || wd == -1);
+    wsum += wr + wd;
   }
+  const bool wraps = act && c0 + vb == cols;  // the chunk holds the row's last column
+  const int t0 = blockIdx.y * slab, t1 = min(T, t0 + slab);
+  for (int t = t0; t < t1; t++) {
+    const uint8_t *bt = bits + (size_t)t * nbytes;
+    long long c = 0;
+    if (act) {
+      const int off = r * cols + c0;
+      const uint32_t X = stream32(bt, nbytes, off);
+      uint32_t R = stream32(bt, nbytes, off + 1);
+      if (wraps) {  // right neighbour of the last column is column 0 of the row
+        const uint32_t first = stream32(bt, nbytes, r * cols) >> 31;
+        const int pos = 32 - vb;  // bit of the last valid column
+        R = (R & ~(1u << pos)) | (first << pos);
+      }
+      const uint32_t D = stream32(bt, nbytes, rd * cols + c0);
+      if (unit) {
+        const uint32_t xr = (X ^ R) & valid, xd = (X ^ D) & valid;
+        c = __popc(xr & ~negR) - __popc(xr & negR) + __popc(xd & ~negD) - __popc(xd & negD);
+      } else {
+        for (int b = 0; b < vb; b++) {
+          const int x = r * cols + c0 + b;
+          const uint32_t m = 1u << (31 - b);
+          if ((X ^ R) & m) c += w[2 * x];
+          if ((X ^ D) & m) c += w[2 * x + 1];
+        }
+      }
+    }
+    long long ws = wsum;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    c += __shfl_xor_sync(0xffffffffu, c, o);
-    e += __shfl_xor_sync(0xffffffffu, e, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicAdd(cut + blockIdx.y, (unsigned long long)c);
-    atomicAdd(energy + blockIdx.y, (unsigned long long)e);
+    for (int o = 16; o > 0; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // energy = W - 2 cut: reduce c and (ws - 2c) over the block
+    if (lane == 0) red[warp] = c;
+    __syncthreads();
+    long long cb = 0;
+    if (threadIdx.x < 8) cb = red[threadIdx.x];
+    __syncthreads();
+    if (lane == 0) red[warp] = ws;
+    __syncthreads();
+    long long wb = 0;
+    if (threadIdx.x < 8) wb = red[threadIdx.x];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        cb += __shfl_xor_sync(0xffffffffu, cb, o);
+        wb += __shfl_xor_sync(0xffffffffu, wb, o);
+      }
+      if (lane == 0) {
+        atomicAdd(cut + t, (unsigned long long)cb);
+        atomicAdd(energy + t, (unsigned long long)(wb - 2 * cb));
+      }
+    }
   }
 }
 
@@ -72,10 +155,17 @@ int torus_cut_energy(int rows, int cols, const int8_t *w, const uint8_t *bits, i
   if (cudaMemsetAsync(cut, 0, sizeof(int64_t) * T, stream) != cudaSuccess ||
       cudaMemsetAsync(energy, 0, sizeof(int64_t) * T, stream) != cudaSuccess)
     return set_error(GSB_ECUDA, "memset failed");
-  int bx = (n + 255) / 256;
-  if (bx > 1024) bx = 1024;
-  dim3 grid(bx, T);
-  torus_cut_energy_kernel<<<grid, 256, 0, stream>>>(rows, cols, w, bits, (n + 7) / 8,
+  const int WPR = (cols + 31) / 32;
+  const int bx = (rows * WPR + 255) / 256;
+  // trials per block: enough blocks to fill the SMs, slabs as long as that allows
+  // (a thread builds its chunk's sign planes once per slab)
+  int slabs = (2 * num_sms() + bx - 1) / bx;
+  if (slabs < 1) slabs = 1;
+  if (slabs > T) slabs = T;
+  if (slabs > 65535) slabs = 65535;
+  const int slab = (T + slabs - 1) / slabs;
+  dim3 grid(bx, (T + slab - 1) / slab);
+  torus_cut_energy_kernel<<<grid, 256, 0, stream>>>(rows, cols, WPR, w, bits, (n + 7) / 8, T, slab,
                                                     (unsigned long long *)cut,
                                                     (unsigned long long *)energy);
   cudaError_t e = cudaGetLastError();

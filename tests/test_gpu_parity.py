@@ -382,3 +382,37 @@ def test_threshold_extremes(oracle, t0, t1):
             for i in range(len(seeds)):
                 assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
                     ref[0][i], ref[2][i], oracle.encode_hex(ref[1][i])), (kind, eng, i)
+
+
+def test_torus_evaluator_any_int8_weights_and_shapes():
+    """gsb_torus_cut_energy (the bit-sliced popcount evaluator, per-site path for
+    chunks with non-unit weights) against a numpy evaluation of evaluate.py:35-49
+    on tori of awkward widths, +-1 and general int8 weights, many trials."""
+    from paper_2505_18508_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(3)
+    for (R, C, T, unit) in [(3, 3, 5, True), (4, 33, 9, True), (7, 100, 70, True), (5, 64, 3, False),
+                            (6, 95, 40, False), (100, 140, 300, True), (9, 31, 17, False)]:
+        n = R * C
+        w = (rng.integers(0, 2, 2 * n) * 2 - 1).astype(np.int8) if unit else \
+            rng.integers(-7, 8, 2 * n).astype(np.int8)
+        if not unit:
+            w[: 2 * C] = (rng.integers(0, 2, 2 * C) * 2 - 1)  # one all-unit row: both paths
+        spins = rng.integers(0, 2, (T, n)).astype(np.uint8)
+        bits = np.packbits(spins, axis=1)
+        s = spins.astype(np.int64).reshape(T, R, C) * 2 - 1
+        wr = w[0::2].astype(np.int64).reshape(R, C)
+        wd = w[1::2].astype(np.int64).reshape(R, C)
+        right, down = np.roll(s, -1, axis=2), np.roll(s, -1, axis=1)
+        cut = ((s != right) * wr + (s != down) * wd).sum(axis=(1, 2))
+        energy = (s * right * wr + s * down * wd).sum(axis=(1, 2))
+        wt = torch.from_numpy(w).cuda()
+        bt = torch.from_numpy(bits).cuda()
+        c = torch.empty(T, dtype=torch.int64, device="cuda")
+        e = torch.empty(T, dtype=torch.int64, device="cuda")
+        ts = _lib.torus_struct(R, C, wt.data_ptr())
+        _lib.check(L.gsb_torus_cut_energy(ts, bt.data_ptr(), T, c.data_ptr(), e.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream))
+        assert c.cpu().numpy().tolist() == cut.tolist(), (R, C)
+        assert e.cpu().numpy().tolist() == energy.tolist(), (R, C)
