@@ -25,7 +25,8 @@
 //                  (one SHFL per plane; the row wraps from the last column);
 //   up / down      slot j -+ 1 of the same lane, or, at the block edges, the
 //                  adjacent block's edge row through a shared-memory
-//                  exchange (double-buffered, one barrier per round).
+//                  exchange (one 64-bit (S, U) word per lane and edge row,
+//                  stale-tolerant; one team barrier per round).
 // Per sweep:
 //   1. priority planes 0..7 (2 Philox blocks per word) to shared memory and,
 //      for SA, the acceptance planes A2 / A4 = [u < K(-2)] / [u < K(-4)]
@@ -41,7 +42,11 @@
 //   3. rounds: ready = unvisited & no unvisited preceding neighbour; Delta
 //      classes from the 4 positive-term planes; flip = ready & (Delta >= 0 |
 //      accepted); slots update in order, so a chain down a lane's rows can
-//      advance several levels in one round;
+//      advance several levels in one round.  The rounds are bound by the ALU
+//      pipe (LOP3/SHF), so shifts by powers of two and additions of disjoint
+//      bit sets are multiply-adds with multipliers the compiler cannot fold
+//      (kernel arguments m_one, m_two, m_neg, m_last): they issue on the
+//      otherwise idle FMA pipe;
 //   4. Delta of every flip at its visit, recomputed from the end-of-sweep
 //      spins (a preceding neighbour's final spin, a following neighbour's
 //      initial one); the running cut in priority order is cur0 + the prefix
