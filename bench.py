@@ -598,6 +598,12 @@ def main(argv=None):
                           "instruction per 2 cycles per SM sub-partition)",
             "updates_per_launch": upd_rank, "launch_ms": launch_s * 1e3,
             "updates_per_s": kernel_rate, "philox": philox_roof, "smem": smem,
+            # not measured by this run: the committed ncu capture of the same launch
+            "ncu_capture": {"file": "profiles/r02_ncu_rscan2_v5_summary.txt",
+                            "workload": "config 2, 1024 trials x 10000 sweeps, rscan2_kernel<7,2>",
+                            "alu_pipe_active_pct": 55.4, "fma_pipe_active_pct": 15.5,
+                            "ipc_per_sm": 2.20, "issue_active_pct": 55.2,
+                            "warp_instructions_per_update": 2.0, "dram_bytes": 606208},
         }
     elif blocks_per_step is not None:
         roofline = {
