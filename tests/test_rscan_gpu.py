@@ -210,3 +210,19 @@ def test_checkerboard_order_shifts_the_distribution():
     c = _final_cuts(inst, ANNEALING_CHECKERBOARD, 1000, 1024)
     se = np.sqrt(a.var(ddof=1) / len(a) + c.var(ddof=1) / len(c))
     assert c.mean() - a.mean() > 4 * se
+
+
+def test_random_scan_sizes_interleaved_in_one_process(oracle):
+    """The same kernel instantiation launched with different shared-memory
+    sizes in one process (large torus, small torus, large again): regression
+    for a cached occupancy whose MaxDynamicSharedMemorySize had been lowered."""
+    try:
+        _test_rscan_shape(8, 7)
+        big = generate_torus(TorusSpec(56, 1000, 1))
+        small = generate_torus(TorusSpec(50, 64, 2))
+        seeds = mix_seeds(MASTER, range(2))
+        cfg = default_config(ANNEALING_RANDOM_SCAN, 2, 0)
+        for inst in (big, small, big, small):
+            _check(oracle, inst, cfg, seeds)
+    finally:
+        _test_rscan_shape(0, 0)
