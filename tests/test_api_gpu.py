@@ -253,3 +253,30 @@ def test_integration_ctypes_stub():
     with pytest.raises(ValueError):
         stub.run_trials_torus(TorusSpec(5, 5, 1), "simulated_annealing_checkerboard", 5, [1],
                               3.0, 0.05, engine=1)  # odd torus: GSB_EUNSUPPORTED -> ValueError
+
+
+def test_concurrent_host_threads_get_serial_results():
+    """run_campaign may call run_trial from ThreadPoolExecutor threads
+    (campaign.py:418-424): the ABI is reentrant -- per-call workspaces, a
+    thread-local error message, mutex-guarded property caches.  Eight threads
+    running different kinds and torus sizes at once get the serial results."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2505_18508_b200.solvers import ANNEALING_RANDOM_SCAN, GREEDY_RANDOM_SCAN
+
+    jobs = []
+    for i, (R, C) in enumerate([(8, 8), (20, 30), (50, 100), (12, 64), (100, 100), (30, 34)]):
+        inst = generate_torus(TorusSpec(R, C, i + 1))
+        for kind in (ANNEALING, ANNEALING_CHECKERBOARD, ANNEALING_RANDOM_SCAN, GREEDY_RANDOM_SCAN):
+            if kind == ANNEALING_CHECKERBOARD and (R | C) & 1:
+                continue
+            jobs.append((inst, default_config(kind, 15, 0), [int(s) for s in range(i + 3, i + 9)]))
+    serial = [run_trials(*j) for j in jobs]
+
+    def work(j):
+        return run_trials(*j)
+
+    with ThreadPoolExecutor(8) as pool:
+        for rep in range(3):
+            for s, p in zip(serial, pool.map(work, jobs)):
+                assert np.array_equal(s.best_cut, p.best_cut) and np.array_equal(s.bits, p.bits)
