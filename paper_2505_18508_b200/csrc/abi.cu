@@ -39,6 +39,33 @@ int num_sms() {
   return cache[dev];
 }
 
+cudaError_t allow_dynamic_smem(const void *kern, size_t bytes) {
+  struct Entry {
+    int dev;
+    const void *kern;
+    size_t max_bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> seen;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  Entry *hit = nullptr;
+  for (auto &en : seen)
+    if (en.dev == dev && en.kern == kern) hit = &en;
+  if (hit && hit->max_bytes >= bytes) return cudaSuccess;
+  if (bytes > 48 * 1024 || hit) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+  }
+  if (hit)
+    hit->max_bytes = bytes;
+  else
+    seen.push_back(Entry{dev, kern, bytes});
+  return cudaSuccess;
+}
+
 static bool torus_ok(const gsb_torus *t) {
   return t && t->rows >= 3 && t->cols >= 3 && t->w_dev &&
          (int64_t)t->rows * t->cols < (int64_t)1 << 30;

@@ -634,11 +634,8 @@ static int launch_nt(const CheckerArgs &a, bool sa, int nsm, cudaStream_t stream
   const size_t smem = smem_bytes(a.nw, NT, WPT);
   auto kern = sa ? checker_sweep_kernel<NT, WPT, true, MINB>
                  : checker_sweep_kernel<NT, WPT, false, MINB>;
-  if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return set_error(GSB_ECUDA, "cudaFuncSetAttribute failed");
-  }
+  if (allow_dynamic_smem((const void *)kern, smem) != cudaSuccess)
+    return set_error(GSB_ECUDA, "cudaFuncSetAttribute failed");
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess ||
       per_sm < 1)

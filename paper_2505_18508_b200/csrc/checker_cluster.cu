@@ -704,8 +704,7 @@ size_t checker_cluster_workspace_bytes(int rows, int cols) {
 template <int WPT, bool SA>
 static int cl_configure(int C, size_t smem, int *max_clusters) {
   auto kern = checker_cluster_kernel<WPT, SA>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  if (allow_dynamic_smem((const void *)kern, smem) != cudaSuccess)
     return set_error(GSB_ECUDA, "cudaFuncSetAttribute(smem) failed");
   if (C > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
                    cudaSuccess)

@@ -558,9 +558,7 @@ int checker_hbm_run(int rows, int cols, const int8_t *w_dev, int kind, int sweep
     const int tw = (nw + g - 1) / g;
     const size_t s = (size_t)tw * 16 * 3 + (size_t)tw * 4 * (1 + HBM_MAX_T) + 16;
     if (s > 200 * 1024) continue;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s) !=
-        cudaSuccess)
-      continue;
+    if (allow_dynamic_smem((const void *)kern, s) != cudaSuccess) continue;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, HBM_NT, s) != cudaSuccess)
       continue;

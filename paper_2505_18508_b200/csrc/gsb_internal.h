@@ -11,6 +11,11 @@ namespace gsb {
 
 int set_error(int code, const char *msg);
 int num_sms();
+// Allow `kern` at least `bytes` of dynamic shared memory on the current device.
+// The limit is only ever raised and the bookkeeping is mutex-guarded: host
+// threads launching the same instantiation for tori of different sizes cannot
+// lower it under each other.  Returns cudaSuccess or the CUDA error.
+cudaError_t allow_dynamic_smem(const void *kern, size_t bytes);
 
 // checkerboard engine (checker.cu)
 int checker_words(int rows, int cols, int *WPR, int *nw);

@@ -500,9 +500,7 @@ int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.err = err_ws;
   const size_t smem = ref_warp_smem(n);
   auto kern = ref_warp_kernel<true>;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
+  if (allow_dynamic_smem((const void *)kern, smem) != cudaSuccess)
     return set_error(GSB_ECUDA, "cudaFuncSetAttribute failed");
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, smem) !=

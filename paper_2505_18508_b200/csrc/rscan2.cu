@@ -66,9 +66,7 @@ static bool rs2_blocks(int rows, int RB, int maxblocks, int &NBu, int &nbig) {
 }
 
 // resident CTAs per SM of an instantiation at a dynamic shared memory size
-// (cached; -1 = does not fit).  The kernel's MaxDynamicSharedMemorySize
-// attribute is only ever raised: tori of different sizes launch the same
-// instantiation with different sizes in one process.
+// (cached; -1 = does not fit)
 static int rs2_occupancy(int nw, int rb, bool sa, size_t smem) {
   static std::mutex mu;
   struct Key {
@@ -76,45 +74,26 @@ static int rs2_occupancy(int nw, int rb, bool sa, size_t smem) {
     size_t smem;
     int occ;
   };
-  struct Attr {
-    int dev, nw, rb, sa;
-    size_t max_smem;
-  };
   static Key cache[512];
   static int ncache = 0;
-  static Attr attrs[512];
-  static int nattrs = 0;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  const void *kern = rs2_kernel(nw, rb, sa);
+  if (!kern) return -1;
+  // every call: the limit may have to rise for this size (allow_dynamic_smem)
+  if (allow_dynamic_smem(kern, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
   std::lock_guard<std::mutex> lk(mu);
   for (int i = 0; i < ncache; i++)
     if (cache[i].dev == dev && cache[i].nw == nw && cache[i].rb == rb && cache[i].sa == (int)sa &&
         cache[i].smem == smem)
       return cache[i].occ;
-  const void *kern = rs2_kernel(nw, rb, sa);
-  if (!kern) return -1;
-  Attr *at = nullptr;
-  for (int i = 0; i < nattrs; i++)
-    if (attrs[i].dev == dev && attrs[i].nw == nw && attrs[i].rb == rb && attrs[i].sa == (int)sa)
-      at = &attrs[i];
-  if (!at && nattrs < 512) {
-    attrs[nattrs] = Attr{dev, nw, rb, (int)sa, 0};
-    at = &attrs[nattrs++];
-  }
-  int occ = -1;
-  bool ok = true;
-  if (!at || smem > at->max_smem) {
-    ok = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-         cudaSuccess;
-    if (ok && at) at->max_smem = smem;
-  }
-  if (ok) {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem) ==
-            cudaSuccess &&
-        per_sm >= 1)
-      occ = per_sm;
-  }
+  int occ = -1, per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nw * 32, smem) == cudaSuccess &&
+      per_sm >= 1)
+    occ = per_sm;
   cudaGetLastError();
   if (ncache < 512) cache[ncache++] = Key{dev, nw, rb, (int)sa, smem, occ};
   return occ;
