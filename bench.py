@@ -270,7 +270,7 @@ def run_reference_arm(a):
         "metric": METRIC,
         "value": v, "unit": "spin-updates/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "higher_is_better": True, "scaling": a.scaling,
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": config_dict(a, world),
         "reference_kind": "simulated_annealing: run_trial's own dynamics (solvers.py:91-140), C "
                           "port on host cores; the same law as the random-scan kind",
@@ -679,7 +679,7 @@ def main(argv=None):
             "value": value, "unit": "spin-updates/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": tot_ms / a.steps, "higher_is_better": True,
-            "scaling": a.scaling, "vs_baseline": None, "dtype": "int32",
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded +-1 torus, generate_torus weights)",
             "config": config_dict(a, world),
             "per_gpu_value": value / world,
