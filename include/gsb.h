@@ -60,6 +60,11 @@ extern "C" {
                                      solvers.py:107-127 with the same law, best-so-far of the
                                      sequential scan exact; tori up to 8 warps x 7 rows per lane */
 
+#define GSB_ENGINE_RANDOM_SCAN_LARGE 5 /* same contract and results as RANDOM_SCAN, forces the
+                                         engine for tori beyond one SM (planes in global
+                                         memory, one cooperative kernel per 8 trials; used
+                                         automatically when the torus exceeds the teams) */
+
 typedef struct gsb_torus {
     int32_t rows, cols;  /* TorusSpec.rows/cols (instances.py:186-187), >= 3 */
     const int8_t *w_dev; /* [rows*cols*2] device pointer, see above           */
@@ -116,8 +121,9 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
                     int64_t *best_cut_dev, int32_t *sweeps_executed_dev, uint8_t *best_bits_dev,
                     void *workspace_dev, size_t workspace_bytes, void *stream);
 
-/* 1 if a rows x cols torus fits the random-scan engine (GSB_ENGINE_RANDOM_SCAN:
- * cols <= 1024 and rows <= 8 * floor(32 / ceil(cols / 32)) * 7), else 0. */
+/* Which random-scan engine a rows x cols torus gets: 1 = the register-resident
+ * teams (cols <= 1024 and rows <= 8 * floor(32 / ceil(cols / 32)) * 7), 2 = the
+ * large-torus engine (n < 2^28), 0 = none. */
 int gsb_rscan_fits(int32_t rows, int32_t cols);
 
 /* Team shape the random-scan engine launches for T trials of a rows x cols

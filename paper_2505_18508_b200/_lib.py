@@ -28,6 +28,7 @@ ENGINE_CHECKERBOARD = 1
 ENGINE_CHECKERBOARD_TILED = 2
 ENGINE_CHECKERBOARD_CLUSTER = 3
 ENGINE_RANDOM_SCAN = 4
+ENGINE_RANDOM_SCAN_LARGE = 5
 
 _lock = threading.Lock()
 _lib = None

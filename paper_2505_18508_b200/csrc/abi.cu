@@ -160,7 +160,8 @@ int gsb_schedule_table(int engine, int32_t sweeps, double t0, double t1, int32_t
   if (engine == GSB_ENGINE_REFERENCE)
     bits = 53;
   else if (engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_TILED ||
-           engine == GSB_ENGINE_CHECKERBOARD_CLUSTER || engine == GSB_ENGINE_RANDOM_SCAN)
+           engine == GSB_ENGINE_CHECKERBOARD_CLUSTER || engine == GSB_ENGINE_RANDOM_SCAN ||
+           engine == GSB_ENGINE_RANDOM_SCAN_LARGE)
     bits = 32;
   else
     return set_error(GSB_EINVAL, "unknown engine");
@@ -181,8 +182,11 @@ size_t gsb_torus_workspace_bytes(const gsb_torus *inst, int engine, int32_t swee
   if (!inst) return 0;
   int n = inst->rows * inst->cols;
   size_t b = err_bytes();
-  if (engine == GSB_ENGINE_RANDOM_SCAN) {
-    // no scratch beyond the error word and counters
+  if (engine == GSB_ENGINE_RANDOM_SCAN || engine == GSB_ENGINE_RANDOM_SCAN_LARGE) {
+    // rscan2 needs no scratch beyond the error word and counters; the large-torus
+    // engine keeps the planes of up to 8 trials in the workspace
+    if (engine == GSB_ENGINE_RANDOM_SCAN_LARGE || !rscan2_fits(inst->rows, inst->cols))
+      b += rscan_big_workspace_bytes(inst->rows, inst->cols, T);
   } else if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
     b += checker_workspace_bytes(inst->rows, inst->cols);
   } else if ((engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_CLUSTER) &&
@@ -248,9 +252,12 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     } else {
       return set_error(GSB_EUNSUPPORTED, "torus too large for the checkerboard engines");
     }
-  } else if (engine == GSB_ENGINE_RANDOM_SCAN) {
+  } else if (engine == GSB_ENGINE_RANDOM_SCAN && rscan2_fits(inst->rows, inst->cols)) {
     rc = rscan2_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
                     sweeps_exec, best_bits, err, (unsigned long long *)((char *)err + 16), stream);
+  } else if (engine == GSB_ENGINE_RANDOM_SCAN || engine == GSB_ENGINE_RANDOM_SCAN_LARGE) {
+    rc = rscan_big_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
+                       best_cut, sweeps_exec, best_bits, rest, err, stream);
   } else if (engine == GSB_ENGINE_REFERENCE && ref_warp_fits(inst->rows, inst->cols)) {
     rc = ref_warp_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
                       sweeps_exec, best_bits, rest, err, stream);
@@ -263,7 +270,9 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
   return rc;
 }
 
-int gsb_rscan_fits(int32_t rows, int32_t cols) { return rscan2_fits(rows, cols) ? 1 : 0; }
+int gsb_rscan_fits(int32_t rows, int32_t cols) {
+  return rscan2_fits(rows, cols) ? 1 : rscan_big_fits(rows, cols) ? 2 : 0;
+}
 
 int gsb_rscan_shape(int32_t rows, int32_t cols, int32_t T, int32_t *warps, int32_t *rows_per_lane) {
   if (!warps || !rows_per_lane) return set_error(GSB_EINVAL, "null argument");

@@ -57,6 +57,14 @@ int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws,
                unsigned long long *stats, cudaStream_t stream);
 
+// random-scan engine for tori beyond rscan2's teams (rscan_big.cu: planes in global memory)
+bool rscan_big_fits(int rows, int cols);
+size_t rscan_big_workspace_bytes(int rows, int cols, int T);
+int rscan_big_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
+                  const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
+                  int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
+                  cudaStream_t stream);
+
 // reference-exact engines (refexact.cu: any graph; refexact_warp.cu: tori, n < 2^16)
 bool ref_warp_fits(int rows, int cols);
 int ref_warp_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,

@@ -166,6 +166,7 @@ _ENGINE_FAMILY = {
     _lib.ENGINE_CHECKERBOARD_TILED: "checkerboard",
     _lib.ENGINE_CHECKERBOARD_CLUSTER: "checkerboard",
     _lib.ENGINE_RANDOM_SCAN: "random_scan",
+    _lib.ENGINE_RANDOM_SCAN_LARGE: "random_scan",
 }
 
 
@@ -178,8 +179,9 @@ def _graph_dmax(instance: ProblemInstance) -> int:
 
 
 def rscan_fits(rows: int, cols: int) -> bool:
-    """Whether a rows x cols torus fits the random-scan engine (register-resident teams)."""
-    return _lib.lib().gsb_rscan_fits(rows, cols) == 1
+    """Whether a rows x cols torus fits a random-scan engine (register-resident teams, or the
+    large-torus engine with its planes in global memory)."""
+    return _lib.lib().gsb_rscan_fits(rows, cols) != 0
 
 
 def rscan_shape(rows: int, cols: int, T: int) -> tuple[int, int]:

@@ -226,3 +226,68 @@ def test_random_scan_sizes_interleaved_in_one_process(oracle):
             _check(oracle, inst, cfg, seeds)
     finally:
         _test_rscan_shape(0, 0)
+
+
+# ---- the large-torus engine (rscan_big.cu): same contract, planes in global memory
+BIG_TORI = [(3, 3, 1), (4, 5, 2), (9, 11, 4), (16, 66, 2), (31, 17, 5), (50, 100, 1), (7, 300, 6),
+            (100, 140, 1), (40, 33, 7), (13, 64, 8), (3, 1100, 9), (70, 1100, 3)]
+
+
+def _check_big(oracle, inst, cfg, seeds, idx=None, engine="large"):
+    from paper_2505_18508_b200 import _lib
+
+    R, C = inst.torus.rows, inst.torus.cols
+    eng = _lib.ENGINE_RANDOM_SCAN_LARGE if engine == "large" else None
+    b = run_trials(inst, cfg, seeds, engine=eng)
+    idx = range(len(seeds)) if idx is None else idx
+    sub = [int(seeds[i]) for i in idx]
+    bc, bs, se = oracle.run_trials_rscan(R, C, inst.torus_weights, cfg.kind, cfg.sweeps, sub,
+                                         cfg.temp_start, cfg.temp_end)
+    for k, i in enumerate(idx):
+        assert (int(b.best_cut[i]), int(b.sweeps_executed[i]), b.hex(i)) == (
+            bc[k], se[k], oracle.encode_hex(bs[k])), (R, C, cfg, i)
+    return b
+
+
+@pytest.mark.parametrize("R,C,s", BIG_TORI)
+def test_large_torus_engine_matches_oracle(oracle, R, C, s):
+    """The large-torus random-scan engine forced on tori of every layout (also
+    beyond 1024 columns, which only it can run), SA and greedy, batches above
+    and below its 8 trials per launch."""
+    inst = generate_torus(TorusSpec(R, C, s))
+    sweeps = 25 if R * C <= 2000 else 6
+    seeds = [int(x) for x in mix_seeds(MASTER, range(9))] + [0, 2**64 - 1]
+    for cfg in (default_config(ANNEALING_RANDOM_SCAN, sweeps, 0),
+                SolverConfig(ANNEALING_RANDOM_SCAN, sweeps, 0, 1.5, 0.2),
+                default_config(GREEDY_RANDOM_SCAN, 100, 0)):
+        _check_big(oracle, inst, cfg, seeds)
+
+
+def test_large_torus_engine_equals_team_engine():
+    """Same contract: the two random-scan engines give identical results."""
+    from paper_2505_18508_b200 import _lib
+
+    inst = generate_torus(TorusSpec(100, 100, 1))
+    seeds = mix_seeds(MASTER, range(20))
+    cfg = default_config(ANNEALING_RANDOM_SCAN, 300, 0)
+    a = run_trials(inst, cfg, seeds)
+    b = run_trials(inst, cfg, seeds, engine=_lib.ENGINE_RANDOM_SCAN_LARGE)
+    assert np.array_equal(a.best_cut, b.best_cut) and np.array_equal(a.bits, b.bits)
+    assert np.array_equal(a.sweeps_executed, b.sweeps_executed)
+
+
+def test_large_torus_engine_threshold_extremes(oracle):
+    inst = generate_torus(TorusSpec(8, 13, 3))
+    seeds = [int(x) for x in mix_seeds(MASTER, range(5))]
+    for t0, t1 in [(1e12, 1e11), (1e-2, 1e-3)]:
+        _check_big(oracle, inst, SolverConfig(ANNEALING_RANDOM_SCAN, 9, 0, t0, t1), seeds)
+
+
+def test_config5_random_scan_matches_oracle(oracle):
+    """BASELINE config 5 (2000x2000, 4M spins) with the reference-law kind:
+    the default engine for this size against the oracle, 3 trials x 3 sweeps
+    SA (every sweep improves the best at this temperature) and greedy."""
+    inst = generate_torus(TorusSpec(2000, 2000, 1))
+    seeds = [int(x) for x in mix_seeds(MASTER, range(3))]
+    _check_big(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, 3, 0), seeds, engine=None)
+    _check_big(oracle, inst, default_config(GREEDY_RANDOM_SCAN, 2, 0), seeds[:2], engine=None)
