@@ -30,6 +30,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 
 #include "rscan2_kernel.cuh"
 
@@ -60,6 +61,7 @@ struct RbgArgs {
   unsigned long long *hist;               // [T][256] (positive sum << 32) + sum
   int *cb;                                // [T][256] running cut at each bucket start
   int *hcnt, *loff, *lfill;               // [T][256] events per bucket, list offset, fill count
+  int *resb;                              // [T][256][4] per candidate bucket: first maximum, key, id
   uint32_t *cmask;                        // [T][8] candidate buckets
   unsigned long long *list;               // [T][n] events of the candidate buckets
   uint32_t *stream;                       // [T][nstream] output staging
@@ -78,9 +80,13 @@ struct RbgShared {
   uint32_t kstar[RBG_MAXT], idstar[RBG_MAXT];
   uint32_t u1q[RBG_MAXT][4], vq[RBG_MAXT][4];
   int part[RBG_MAXT][4];
-  // step E, one CTA per trial
-  int hsum[4][256], hpos[4][256], hstart[4][256];
-  unsigned long long sortbuf[RBG_SORT];
+  union {
+    struct {  // step E4, one CTA per trial
+      int hsum[4][256], hpos[4][256], hstart[4][256];
+      unsigned long long sortbuf[RBG_SORT];
+    };
+    int priv[3][RBG_MAXT][256];  // step E1: this CTA's bucket sums, positive sums, counts
+  };
   int cnt, e_best, e_improved;
   uint32_t e_key, e_id;
   int scan_carry;
@@ -153,7 +159,15 @@ __device__ void rbg_segment(RbgShared &sh, const unsigned long long *list, int m
   if (tid == 0) sh.cnt = 0;
   __syncthreads();
   int c = 0;
-  for (int i = tid; i < m; i += RBG_NT) c += match(ld64(list + i));
+  {
+    int i = tid;
+    for (; i + 3 * RBG_NT < m; i += 4 * RBG_NT) {  // four loads in flight
+      const unsigned long long e0 = ld64(list + i), e1 = ld64(list + i + RBG_NT);
+      const unsigned long long e2 = ld64(list + i + 2 * RBG_NT), e3 = ld64(list + i + 3 * RBG_NT);
+      c += match(e0) + match(e1) + match(e2) + match(e3);
+    }
+    for (; i < m; i += RBG_NT) c += match(ld64(list + i));
+  }
   c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
   if ((tid & 31) == 0 && c) atomicAdd(&sh.cnt, c);
   __syncthreads();
@@ -251,6 +265,9 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
   const int G = gridDim.x, nw = a.nw, T = a.T, cols = a.cols, WPR = a.WPR;
   const long long items = (long long)T * nw;
   const long long gtid = (long long)blockIdx.x * RBG_NT + tid, gstride = (long long)G * RBG_NT;
+  // CTA c walks the contiguous items [fbeg, fend) of the (trial, word) space: a band of
+  // rows of (mostly) one trial, so neighbours and bucket sums stay local to the CTA
+  const long long fbeg = items * blockIdx.x / G, fend = items * (blockIdx.x + 1) / G;
 
   if (tid < T) {
     sh.seed[tid] = a.seeds[tid];
@@ -291,7 +308,7 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
   grid.sync();
 
   // ---- initial spins: bit b of word 0 of Philox(key, (wi, 0, 31, TAG))
-  for (long long f = gtid; f < items; f += gstride) {
+  for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
     const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
     const uint64_t seed = sh.seed[tr];
     const RbgGeo g = rbg_geo(a, w);
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
   auto cut_pass = [&](bool su) {
     if (tid < T) sh.part[tid][0] = 0;
     __syncthreads();
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       const RbgGeo g = rbg_geo(a, w);
       const size_t o = (size_t)tr * nw;
@@ -331,6 +348,18 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
   }
   __syncthreads();
 
+#ifdef RBG_PROF
+  long long pf[12] = {0}, pf_t = clock64();
+  long long pf_rounds = 0, pf_gated = 0, pf_cand = 0;
+#define RBG_TICK(i)                   \
+  do {                                \
+    const long long now_ = clock64(); \
+    pf[i] += now_ - pf_t;             \
+    pf_t = now_;                      \
+  } while (0)
+#else
+#define RBG_TICK(i)
+#endif
   for (int t = 0; t < a.sweeps; t++) {
     // every CTA holds the same per-trial state; stop when no trial is active
     int anyact = 0;
@@ -364,7 +393,7 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
     __syncthreads();
 
     // ---- A. priority planes, acceptance planes, U = all, S0 = S
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.active[tr]) continue;
       const uint64_t seed = sh.seed[tr];
@@ -411,13 +440,14 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       a.SU[f] = (unsigned long long)s | ((unsigned long long)g.V << 32);
     }
     grid.sync();
+    RBG_TICK(0);
 
     // ---- B. precedence planes Pr, Pd
     // (step E's results of the previous sweep have been read by every CTA: the
     // barrier after phase A is behind them)
     if (blockIdx.x == 0)
       for (int i = tid; i < T * 8; i += RBG_NT) a.res[i] = 0;
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.active[tr]) continue;
       const uint64_t seed = sh.seed[tr];
@@ -466,9 +496,10 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       a.Pd[f] = pd;
     }
     grid.sync();
+    RBG_TICK(1);
 
     // ---- C. Pl(v) = !Pr(left(v)), Pu(v) = !Pd(up(v))
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.active[tr]) continue;
       const RbgGeo g = rbg_geo(a, w);
@@ -478,6 +509,7 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       a.Pu[f] = ~ld32(a.Pd + o + g.up);
     }
     grid.sync();
+    RBG_TICK(2);
 
     // ---- rounds
     for (int rr = 0;; rr++) {
@@ -485,10 +517,13 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
         if (gtid == 0) atomicExch(a.err, GSB_EUNSUPPORTED);
         break;
       }
+#ifdef RBG_PROF
+      pf_rounds++;
+#endif
       int *flag = a.flags + (rr % 3) * T;
       if (blockIdx.x == 0 && tid < T) a.flags[((rr + 1) % 3) * T + tid] = 0;
       uint32_t leftmask = 0;
-      for (long long f = gtid; f < items; f += gstride) {
+      for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
         const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
         if (!sh.active[tr]) continue;
         const unsigned long long su = ld64(a.SU + f);
@@ -537,10 +572,11 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       if (!any) break;
     }
 
+    RBG_TICK(3);
     // ---- D. Delta of every flip at its visit, sums
     if (tid < T) sh.part[tid][0] = sh.part[tid][1] = sh.part[tid][2] = 0;
     __syncthreads();
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.active[tr]) continue;
       const size_t o = (size_t)tr * nw;
@@ -614,10 +650,11 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
     }
     __syncthreads();
     for (int tr = 0; tr < T; tr++) anygated |= sh.gated[tr];
+    RBG_TICK(4);
 
     if (!SA) {
       // greedy: Delta > 0 flips only, the best is the end-of-sweep state
-      for (long long f = gtid; f < items; f += gstride) {
+      for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
         const int tr = (int)(f / nw);
         if (sh.flipped[tr]) a.BS[f] = (uint32_t)ld64(a.SU + f);
       }
@@ -625,8 +662,11 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
     }
     if (!anygated) continue;
 
-    // ---- E1. bucket sums by priority top byte
-    for (long long f = gtid; f < items; f += gstride) {
+    // ---- E1. bucket sums by priority top byte: per CTA in shared memory, then
+    // one global atomic per touched (trial, bucket)
+    for (int i = tid; i < 3 * RBG_MAXT * 256; i += RBG_NT) (&sh.priv[0][0][0])[i] = 0;
+    __syncthreads();
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.gated[tr]) continue;
       const uint4 e = a.EV[f];
@@ -641,13 +681,25 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
         const int b = __ffs(any) - 1;
         any &= any - 1;
         const uint32_t key8 = gather8(pa, pb, b);
-        const long long mag = 2 + 2 * (long long)((M4 >> b) & 1u);
-        const long long v = ((PM >> b) & 1u) ? (mag << 32) + mag : -mag;
-        atomicAdd(&a.hist[(size_t)tr * 256 + key8], (unsigned long long)v);
-        atomicAdd(&a.hcnt[tr * 256 + key8], 1);
+        const int mag = 2 + 2 * (int)((M4 >> b) & 1u);
+        const bool pos = (PM >> b) & 1u;
+        atomicAdd(&sh.priv[0][tr][key8], pos ? mag : -mag);
+        if (pos) atomicAdd(&sh.priv[1][tr][key8], mag);
+        atomicAdd(&sh.priv[2][tr][key8], 1);
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < T * 256; i += RBG_NT) {
+      const int tr = i >> 8, bk = i & 255;
+      const int cntv = sh.priv[2][tr][bk];
+      if (cntv) {
+        const long long v = ((long long)sh.priv[1][tr][bk] << 32) + (long long)sh.priv[0][tr][bk];
+        atomicAdd(&a.hist[(size_t)tr * 256 + bk], (unsigned long long)v);
+        atomicAdd(&a.hcnt[tr * 256 + bk], cntv);
       }
     }
     grid.sync();
+    RBG_TICK(5);
 
     // ---- E2. bucket starts, E, candidates (CTA tr, warp 0)
     if (blockIdx.x < T && sh.gated[blockIdx.x] && tid < 32) {
@@ -714,9 +766,10 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       }
     }
     grid.sync();
+    RBG_TICK(6);
 
     // ---- E3. events of the candidate buckets with their full keys
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.gated[tr] || __ldcg(&a.res[tr * 8]) == 0) continue;
       const uint4 e = a.EV[f];
@@ -744,47 +797,71 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       }
     }
     grid.sync();
+    RBG_TICK(7);
 
-    // ---- E4. the first maximum of the running cut (CTA tr)
-    if (blockIdx.x < T && sh.gated[blockIdx.x] && __ldcg(&a.res[blockIdx.x * 8]) > 0) {
-      const int tr = blockIdx.x;
-      const int E = __ldcg(&a.res[tr * 8 + 1]);
-      if (tid == 0) {
-        sh.e_best = sh.best[tr];
-        sh.e_improved = 0;
-        sh.e_key = sh.e_id = 0u;
-      }
-      __syncthreads();
-      const unsigned long long *L = a.list + (size_t)tr * a.n;
-      for (int bkt = 0; bkt < 256; bkt++) {
-        if (!((__ldcg(&a.cmask[tr * 8 + (bkt >> 5)]) >> (bkt & 31)) & 1u)) continue;
-        const unsigned long long x = __ldcg(&a.hist[(size_t)tr * 256 + bkt]);
-        const int sbv = (int)(uint32_t)x;
-        const int pbv = (int)((long long)(x - (unsigned long long)(long long)sbv) >> 32);
-        const int base = __ldcg(&a.cb[tr * 256 + bkt]);
-        if (base + pbv < max(sh.e_best + 1, E)) continue;
-        rbg_segment(sh, L + __ldcg(&a.loff[tr * 256 + bkt]), __ldcg(&a.hcnt[tr * 256 + bkt]), 8,
-                    (uint32_t)bkt << 24, base, E, 0, a.err);
-        __syncthreads();
-      }
-      if (tid == 0) {
-        a.res[tr * 8 + 2] = sh.e_best;
-        a.res[tr * 8 + 3] = (int)sh.e_key;
-        a.res[tr * 8 + 4] = (int)sh.e_id;
-        a.res[tr * 8 + 5] = sh.e_improved;
+    // ---- E4. the first maximum of the running cut.  Every candidate bucket is an
+    // independent task (its start value is known): task k goes to CTA k mod G,
+    // which finds the bucket's own first maximum above the best before this
+    // sweep; the buckets' results are then combined in bucket order (strict
+    // improvement), which is the sequential scan's first attainment.
+    {
+      int k = 0;
+      for (int tr = 0; tr < T; tr++) {
+        if (!sh.gated[tr] || __ldcg(&a.res[tr * 8]) == 0) continue;
+        const int E = __ldcg(&a.res[tr * 8 + 1]);
+        const unsigned long long *L = a.list + (size_t)tr * a.n;
+        for (int q = 0; q < 8; q++) {
+          uint32_t mw = __ldcg(&a.cmask[tr * 8 + q]);
+          while (mw) {
+            const int bkt = 32 * q + __ffs(mw) - 1;
+            mw &= mw - 1;
+            if (k++ % G != (int)blockIdx.x) continue;
+            if (tid == 0) {
+              sh.e_best = sh.best[tr];
+              sh.e_improved = 0;
+              sh.e_key = sh.e_id = 0u;
+            }
+            __syncthreads();
+            rbg_segment(sh, L + __ldcg(&a.loff[tr * 256 + bkt]), __ldcg(&a.hcnt[tr * 256 + bkt]), 8,
+                        (uint32_t)bkt << 24, __ldcg(&a.cb[tr * 256 + bkt]), E, 0, a.err);
+            __syncthreads();
+            if (tid == 0) {
+              int *rb = a.resb + (tr * 256 + bkt) * 4;
+              rb[0] = sh.e_improved ? sh.e_best : INT_MIN;
+              rb[1] = (int)sh.e_key;
+              rb[2] = (int)sh.e_id;
+            }
+            __syncthreads();
+          }
+        }
       }
     }
     grid.sync();
+    RBG_TICK(8);
 
     // ---- E5. snapshot: S0 ^ (flips with (priority, id) <= (key*, id*))
-    if (tid < T && sh.gated[tid] && __ldcg(&a.res[tid * 8 + 5])) {
-      sh.improved[tid] = 1;
-      sh.best[tid] = __ldcg(&a.res[tid * 8 + 2]);
-      sh.kstar[tid] = (uint32_t)__ldcg(&a.res[tid * 8 + 3]);
-      sh.idstar[tid] = (uint32_t)__ldcg(&a.res[tid * 8 + 4]);
+    if (tid < T && sh.gated[tid] && __ldcg(&a.res[tid * 8]) > 0) {
+      const int tr = tid;
+      int bst = sh.best[tr];
+      for (int q = 0; q < 8; q++) {
+        uint32_t mw = __ldcg(&a.cmask[tr * 8 + q]);
+        while (mw) {
+          const int bkt = 32 * q + __ffs(mw) - 1;
+          mw &= mw - 1;
+          const int *rb = a.resb + (tr * 256 + bkt) * 4;
+          const int mval = __ldcg(rb);
+          if (mval > bst) {
+            bst = mval;
+            sh.kstar[tr] = (uint32_t)__ldcg(rb + 1);
+            sh.idstar[tr] = (uint32_t)__ldcg(rb + 2);
+            sh.improved[tr] = 1;
+          }
+        }
+      }
+      sh.best[tr] = bst;
     }
     __syncthreads();
-    for (long long f = gtid; f < items; f += gstride) {
+    for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
       if (!sh.improved[tr]) continue;
       const uint32_t s = (uint32_t)ld64(a.SU + f), fl = ld32(a.S0 + f) ^ s;
@@ -819,7 +896,19 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
       a.BS[f] = s ^ fl ^ inc;
     }
     // (the next sweep's phase A does not touch BS; its first barrier orders the rest)
+    RBG_TICK(9);
   }
+#ifdef RBG_PROF
+  if (blockIdx.x == 0 && tid == 0) {
+    long long tot = 0;
+    for (int i = 0; i < 12; i++) tot += pf[i];
+    printf("rbg prof (cycles %%): A %.1f B %.1f C %.1f rounds %.1f D %.1f E1 %.1f E2 %.1f E3 %.1f E4 %.1f "
+           "E5 %.1f | total %lld cycles, rounds %lld\n",
+           100.0 * pf[0] / tot, 100.0 * pf[1] / tot, 100.0 * pf[2] / tot, 100.0 * pf[3] / tot,
+           100.0 * pf[4] / tot, 100.0 * pf[5] / tot, 100.0 * pf[6] / tot, 100.0 * pf[7] / tot,
+           100.0 * pf[8] / tot, 100.0 * pf[9] / tot, tot, pf_rounds);
+  }
+#endif
 
   // ---- integrity guard (solvers.py:132-133) and outputs
   grid.sync();
@@ -827,7 +916,7 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
   for (long long i = gtid; i < (long long)T * a.nstream; i += gstride) a.stream[i] = 0u;
   grid.sync();
   cut_pass(false);
-  for (long long f = gtid; f < items; f += gstride) {
+  for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
     const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
     const RbgGeo g = rbg_geo(a, w);
     const uint32_t x = __brev(ld32(a.BS + f) & g.V);
@@ -882,6 +971,7 @@ static size_t rbg_layout(int rows, int cols, int T, RbgArgs *a, char *base) {
   char *acc = take((size_t)3 * TB * 4 * 4), *flags = take((size_t)3 * TB * 4), *res = take((size_t)TB * 8 * 4);
   char *hist = take((size_t)TB * 256 * 8), *cb = take((size_t)TB * 256 * 4), *cmask = take((size_t)TB * 8 * 4);
   char *hcnt = take((size_t)TB * 256 * 4), *loff = take((size_t)TB * 256 * 4), *lfill = take((size_t)TB * 256 * 4);
+  char *resb = take((size_t)TB * 256 * 4 * 4);
   char *list = take((size_t)TB * n * 8);
   char *stream = take((size_t)TB * nstream * 4);
   char *cutacc = take((size_t)TB * 8);
@@ -910,6 +1000,7 @@ static size_t rbg_layout(int rows, int cols, int T, RbgArgs *a, char *base) {
     a->hcnt = (int *)hcnt;
     a->loff = (int *)loff;
     a->lfill = (int *)lfill;
+    a->resb = (int *)resb;
     a->cmask = (uint32_t *)cmask;
     a->list = (unsigned long long *)list;
     a->stream = (uint32_t *)stream;

@@ -7,7 +7,7 @@ from paper_2505_18508_b200.solvers import default_config, run_trials_device
 CFG = {"c1": (50, 100, 100, 1000), "c2": (100, 100, 1024, 1000), "c2full": (100, 100, 1024, 10000),
        "c3": (100, 140, 4096, 300), "c4": (100, 200, 8192, 100), "c2x148": (100, 100, 148, 1000),
        "c2x2048": (100, 100, 2048, 1000), "c5x8": (2000, 2000, 8, 100), "c5": (2000, 2000, 64, 100),
-       "c5x1": (2000, 2000, 1, 100)}
+       "c5x1": (2000, 2000, 1, 100), "c5x8full": (2000, 2000, 8, 1000)}
 kind = sys.argv[1]
 for name in (sys.argv[2:] or ["c1", "c2", "c3", "c4"]):
     R, C, T, S = CFG[name]
