@@ -49,7 +49,8 @@ CONFIGS = {
     "c2": (100, 100, 1024, 10_000),
     "c3": (100, 140, 4096, 20_000),
     "c4": (100, 200, 8192, 50_000),
-    # configs[4]: beyond one SM -> checkerboard kinds only (cluster engine)
+    # configs[4]: beyond one SM -> the large-torus random-scan engine (planes in global
+    # memory, 8 trials per cooperative kernel) / the checkerboard cluster engine
     "c5": (2000, 2000, 64, 1000),
 }
 MASTER = 20250814
@@ -76,8 +77,8 @@ def parse(argv=None):
     ap.add_argument("--dry-run", action="store_true",
                     help="rendezvous and print the sharding plan only (no kernels; CPU test hook)")
     a = ap.parse_args(argv)
-    if a.kind is None:  # config 5 does not fit the random-scan engine's one-SM teams
-        a.kind = "simulated_annealing_checkerboard" if a.config == "c5" else DEFAULT_KIND
+    if a.kind is None:
+        a.kind = DEFAULT_KIND
     return a
 
 
@@ -385,9 +386,12 @@ def main(argv=None):
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     is_rscan = a.kind in RANDOM_SCAN_KINDS
+    # 2 = the torus is beyond the register-resident teams: large-torus engine (rscan_big.cu)
+    rscan_large = is_rscan and L.gsb_rscan_fits(rows, cols) == 2
     is_checker = a.kind in CHECKERBOARD_KINDS
-    # our kernels per step: [checkerboard: masks + geometry tables +] sweep kernel + best-key kernel
-    launches_per_step = 4 if is_checker else 2
+    # our kernels per step: [checkerboard: masks + geometry tables +] sweep kernel (large-torus
+    # random scan: one cooperative launch per 8 trials) + best-key kernel
+    launches_per_step = 4 if is_checker else ((T + 7) // 8 + 1 if rscan_large else 2)
 
     def sweep_launch():
         _lib.check(L.gsb_torus_sweep(ts, cfg.engine, kind_code, S,
@@ -505,7 +509,7 @@ def main(argv=None):
         blocks_per_step = int(blocks[0])
         unit_def = ("Philox4x32-10 blocks the checkerboard contract requires (2 init + 8 planes "
                     "per word and half-sweep + per-site tail groups), counted by the kernel")
-    elif is_rscan:
+    elif is_rscan and not rscan_large:
         st = np.zeros(4, dtype=np.uint64)
         _lib.check(L.gsb_workspace_rscan_stats(ws.data_ptr(), sp, st.ctypes.data))
         words = rows * ((cols + 31) // 32)
@@ -542,7 +546,9 @@ def main(argv=None):
     lop3_peak = nthr * lpt / (pe0.elapsed_time(pe1) / 1e3)  # LOP3 (thread ops)/s
 
     # ---- roofline of the dominant kernel (the sweep kernel of this torus)
-    if is_rscan:
+    if rscan_large:
+        sweep_kernel = "gsb::rscan_big_kernel"
+    elif is_rscan:
         sweep_kernel = "gsb::rscan2_kernel"
     elif is_checker:
         sweep_kernel = ("gsb::checker_sweep_kernel" if (cols // 2 + 31) // 32 * rows <= 2048
@@ -572,7 +578,25 @@ def main(argv=None):
             "algorithmic_units_per_launch": blocks_per_step, "unit_def": unit_def,
             "peak_basis": "measured live: gsb_philox_bench, SMs x 8 x 256 threads, 2 independent "
                           "Philox4x32-10 blocks in flight per thread, CUDA events"}
-    if is_rscan:
+    if rscan_large:
+        # HBM path: compulsory traffic per sweep with bit-packed state,
+        # 0.25 + 0.25 / k bytes per update for k co-resident trials sharing the couplings
+        k = min(T, 8)
+        b_hbm = 0.25 + 0.25 / k
+        hbm_peak = float(peaks.get("hbm_gbs", 6454.9)) * 1e9
+        roofline = {
+            "bound": "hbm", "unit": "GB/s", "achieved": kernel_rate * b_hbm / 1e9,
+            "peak": hbm_peak / 1e9, "frac": kernel_rate * b_hbm / hbm_peak, "traffic": None,
+            "kernel": sweep_kernel, "algorithmic_bytes_per_update": b_hbm,
+            "unit_def": "compulsory bit-packed traffic of the HBM path, 0.25 + 0.25/k B per update "
+                        f"(k = {k} trials per cooperative launch share the couplings); the engine "
+                        "is bound by grid barriers and L2 latency, not by this roof (DESIGN.md)",
+            "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
+                          else "fallback 6454.9 GB/s (B200_PROFILING.md)",
+            "updates_per_launch": upd_rank, "launch_ms": launch_s * 1e3,
+            "updates_per_s": kernel_rate,
+        }
+    elif is_rscan:
         # ALU-pipe (LOP3/SHF) operations the contract's bit-sliced algorithm needs per
         # 32-site word and sweep:
         #   Philox XOR halves 4 blocks x 16, acceptance compare 8 planes x 2 thresholds x 2,
@@ -632,10 +656,12 @@ def main(argv=None):
     # the other two engines, clearly labelled (skipped above 2.5e11 updates:
     # the bit-exact engine would take minutes on configs 3/4)
     secondary = None
-    if not a.no_secondary and cfg.annealing and n < 65536 and T * S * n <= 2.5e11:
+    if not a.no_secondary and cfg.annealing and T * S * n <= 2.6e11:
         secondary = {}
         others = [k for k in ("simulated_annealing_checkerboard", "simulated_annealing",
                               "simulated_annealing_random_scan") if k != a.kind]
+        if n >= 65536:  # the bit-exact engine runs one thread per trial beyond 2^16 sites
+            others = [k for k in others if k != "simulated_annealing"]
         notes = {
             "simulated_annealing_checkerboard":
                 "Philox + systematic colour order: NOT the reference's law (final cuts higher "

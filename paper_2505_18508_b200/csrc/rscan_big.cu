@@ -80,6 +80,7 @@ struct RbgShared {
   uint32_t kstar[RBG_MAXT], idstar[RBG_MAXT];
   uint32_t u1q[RBG_MAXT][4], vq[RBG_MAXT][4];
   int part[RBG_MAXT][4];
+  uint32_t cm[RBG_MAXT][8];  // candidate bucket masks (step E3)
   union {
     struct {  // step E4, one CTA per trial
       int hsum[4][256], hpos[4][256], hstart[4][256];
@@ -769,9 +770,12 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
     RBG_TICK(6);
 
     // ---- E3. events of the candidate buckets with their full keys
+    if (tid < T * 8) sh.cm[tid >> 3][tid & 7] = __ldcg(&a.cmask[tid]);
+    if (tid < T) sh.part[tid][2] = __ldcg(&a.res[tid * 8]);
+    __syncthreads();
     for (long long f = fbeg + tid; f < fend; f += RBG_NT) {
       const int tr = (int)(f / nw), w = (int)(f - (long long)tr * nw);
-      if (!sh.gated[tr] || __ldcg(&a.res[tr * 8]) == 0) continue;
+      if (!sh.gated[tr] || sh.part[tr][2] == 0) continue;
       const uint4 e = a.EV[f];
       uint32_t any = e.x | e.y | e.z | e.w;
       if (!any) continue;
@@ -787,7 +791,7 @@ __global__ void __launch_bounds__(RBG_NT) rscan_big_kernel(RbgArgs a) {
         const int b = __ffs(any) - 1;
         any &= any - 1;
         const uint32_t key8 = gather8(pa, pb, b);
-        if (!((__ldcg(&a.cmask[tr * 8 + (key8 >> 5)]) >> (key8 & 31u)) & 1u)) continue;
+        if (!((sh.cm[tr][key8 >> 5] >> (key8 & 31u)) & 1u)) continue;
         const uint32_t key = (key8 << 24) | rs2_low24((uint32_t)w, (uint32_t)t, 2u, b, k0, k1);
         const uint32_t code = ((PM >> b) & 1u) * 2u + (((PM ^ ~M4) >> b) & 1u);
         const int slot = __ldcg(&a.loff[tr * 256 + key8]) + atomicAdd(&a.lfill[tr * 256 + key8], 1);

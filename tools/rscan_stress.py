@@ -6,7 +6,7 @@ import sys
 import numpy as np
 sys.path.insert(0, '.')
 from oracle import oracle as O
-from paper_2505_18508_b200 import TorusSpec, generate_torus
+from paper_2505_18508_b200 import TorusSpec, _lib, generate_torus
 from paper_2505_18508_b200.solvers import (SolverConfig, _test_rscan_limits, _test_rscan_shape,
                                            rscan_fits, run_trials)
 
@@ -35,8 +35,11 @@ for it in range(cases):
     if rng.random() < 0.5:
         forced = (int(rng.choice([1, 2, 4, 7, 8])), int(rng.choice([1, 2, 3, 4, 5, 7])))
     _test_rscan_shape(*forced)
+    eng = _lib.ENGINE_RANDOM_SCAN_LARGE if rng.random() < 0.3 else None  # the large-torus engine
+    if eng is not None:
+        forced = ("large",)
     try:
-        b = run_trials(inst, cfg, seeds)
+        b = run_trials(inst, cfg, seeds, engine=eng)
     except ValueError:
         _test_rscan_shape(0, 0)
         forced = (0, 0)
