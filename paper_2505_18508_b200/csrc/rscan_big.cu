@@ -38,7 +38,10 @@ namespace cg = cooperative_groups;
 
 namespace gsb {
 
-constexpr int RBG_NT = 256;
+#ifndef RBG_NTV
+#define RBG_NTV 256
+#endif
+constexpr int RBG_NT = RBG_NTV;
 constexpr int RBG_MAXT = 8;     // trials per cooperative launch
 constexpr int RBG_SORT = 2048;  // events one CTA sorts at once (16 KB of shared memory)
 #ifndef RBG_MINB
