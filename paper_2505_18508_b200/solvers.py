@@ -16,7 +16,8 @@ Kinds:
   reference's random visit order, drawn from Philox as per-site priorities and
   run level by level on the GPU (random-scan contract): the
   reference's dynamics in law, so its final-cut distribution agrees with
-  run_trial's.  Tori that fit one SM.
+  run_trial's.  Any torus (register-resident teams up to one SM, the
+  large-torus engine with its planes in global memory beyond).
 
 Every trial is a deterministic function of (instance, config) and never of
 the batch it runs in.
