@@ -44,6 +44,9 @@ namespace gsb {
 constexpr int RBG_NT = RBG_NTV;
 constexpr int RBG_MAXT = 8;     // trials per cooperative launch
 constexpr int RBG_SORT = 2048;  // events one CTA sorts at once (16 KB of shared memory)
+#ifndef RBG_RPB
+#define RBG_RPB 4  // passes of the rounds per grid barrier (1: -14 %, 2: -5 %, 6-8: +1 %)
+#endif
 #ifndef RBG_MINB
 #define RBG_MINB 3  // resident CTAs per SM (85 registers): 3 measured best (2: -8 %, 4: -3 %)
 #endif
@@ -530,6 +533,12 @@ __global__ void __launch_bounds__(RBG_NT, RBG_MINB) rscan_big_kernel(RbgArgs a) 
       int *flag = a.flags + (rr % 3) * T;
       if (blockIdx.x == 0 && tid < T) a.flags[((rr + 1) % 3) * T + tid] = 0;
       uint32_t leftmask = 0;
+      // RBG_RPB passes over the band per grid barrier: the in-place (S, U) words
+      // tolerate stale reads, so passes need no barrier between them -- the
+      // barrier only serves the end-of-sweep test, and passes over finished
+      // words are cheap
+      for (int pass = 0; pass < RBG_RPB; pass++) {
+      leftmask = 0;
       // four words' (S, U) loaded ahead: most words are finished in the late rounds
       // and cost only this load, so the loads must not queue behind each other
       for (long long f0 = fbeg + tid; f0 < fend; f0 += 4 * RBG_NT) {
@@ -580,6 +589,7 @@ __global__ void __launch_bounds__(RBG_NT, RBG_MINB) rscan_big_kernel(RbgArgs a) 
         }
         if (u) leftmask |= 1u << tr;
         }
+      }
       }
       leftmask = __reduce_or_sync(0xffffffffu, leftmask);
       if (lane == 0)
