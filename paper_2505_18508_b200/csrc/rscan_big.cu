@@ -92,7 +92,7 @@ struct RbgShared {
   uint32_t cm[RBG_MAXT][8];  // candidate bucket masks (step E3)
   union {
     struct {  // step E4, one CTA per trial
-      int hsum[4][256], hpos[4][256], hstart[4][256];
+      int hsum[4][256], hpos[4][256], hstart[4][256], hnum[4][256];
       unsigned long long sortbuf[RBG_SORT];
     };
     int priv[3][RBG_MAXT][256];  // step E1: this CTA's bucket sums, positive sums, counts
@@ -158,31 +158,27 @@ __device__ void rbg_sort(RbgShared &sh, int m) {
 // Updates sh.e_best / e_key / e_id / e_improved with the FIRST position whose
 // running cut exceeds e_best (strictly), scanning in order.  `floor` = a value
 // the running cut is known to reach elsewhere (pruning; >= keeps first attainment).
+// `cnt` = how many entries match (known from the parent's sub-bucket counts).
 __device__ void rbg_segment(RbgShared &sh, const unsigned long long *list, int m, int pb,
-                            uint32_t pv, int base, int floorv, int level, int *err) {
+                            uint32_t pv, int base, int floorv, int level, int cnt, int *err) {
   const int tid = threadIdx.x;
   const int sh_bits = 32 - pb;
   auto match = [&](unsigned long long e) -> bool {
     return pb == 0 || ((uint32_t)(e >> 32) >> sh_bits) == (pv >> sh_bits);
   };
-  // count
-  if (tid == 0) sh.cnt = 0;
-  __syncthreads();
-  int c = 0;
-  {
+  // walk the list with four loads in flight (the passes are bound by L2 latency)
+  auto walk = [&](auto &&fn) {
     int i = tid;
-    for (; i + 3 * RBG_NT < m; i += 4 * RBG_NT) {  // four loads in flight
+    for (; i + 3 * RBG_NT < m; i += 4 * RBG_NT) {
       const unsigned long long e0 = ld64(list + i), e1 = ld64(list + i + RBG_NT);
       const unsigned long long e2 = ld64(list + i + 2 * RBG_NT), e3 = ld64(list + i + 3 * RBG_NT);
-      c += match(e0) + match(e1) + match(e2) + match(e3);
+      fn(e0);
+      fn(e1);
+      fn(e2);
+      fn(e3);
     }
-    for (; i < m; i += RBG_NT) c += match(ld64(list + i));
-  }
-  c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
-  if ((tid & 31) == 0 && c) atomicAdd(&sh.cnt, c);
-  __syncthreads();
-  const int cnt = sh.cnt;
-  __syncthreads();
+    for (; i < m; i += RBG_NT) fn(ld64(list + i));
+  };
   if (cnt == 0) return;
   if (cnt <= RBG_SORT || pb >= 32) {
     if (cnt > RBG_SORT) {  // > 2048 events with equal 32-bit priorities: not supported
@@ -191,10 +187,9 @@ __device__ void rbg_segment(RbgShared &sh, const unsigned long long *list, int m
     }
     if (tid == 0) sh.cnt = 0;
     __syncthreads();
-    for (int i = tid; i < m; i += RBG_NT) {
-      const unsigned long long e = ld64(list + i);
+    walk([&](unsigned long long e) {
       if (match(e)) sh.sortbuf[atomicAdd(&sh.cnt, 1)] = e;
-    }
+    });
     __syncthreads();
     rbg_sort(sh, cnt);
     if (tid < 32) {  // in-order scan by one warp
@@ -236,34 +231,36 @@ __device__ void rbg_segment(RbgShared &sh, const unsigned long long *list, int m
   }
   // descend one key byte
   int *hsum = sh.hsum[level], *hpos = sh.hpos[level], *hstart = sh.hstart[level];
-  for (int i = tid; i < 256; i += RBG_NT) hsum[i] = hpos[i] = 0;
+  int *hnum = sh.hnum[level];
+  for (int i = tid; i < 256; i += RBG_NT) hsum[i] = hpos[i] = hnum[i] = 0;
   __syncthreads();
   const int bsh = sh_bits - 8;
-  for (int i = tid; i < m; i += RBG_NT) {
-    const unsigned long long e = ld64(list + i);
-    if (!match(e)) continue;
+  walk([&](unsigned long long e) {
+    if (!match(e)) return;
     const uint32_t code = (uint32_t)e & 3u;
     const int d = code == 0 ? -4 : code == 1 ? -2 : code == 2 ? 2 : 4;
     const int sb = (int)(((uint32_t)(e >> 32) >> bsh) & 255u);
     atomicAdd(&hsum[sb], d);
     if (d > 0) atomicAdd(&hpos[sb], d);
-  }
+    atomicAdd(&hnum[sb], 1);
+  });
   __syncthreads();
   if (tid == 0) {
     int run = base, emax = INT_MIN;
     for (int i = 0; i < 256; i++) {
       hstart[i] = run;
       run += hsum[i];
-      if (hsum[i] | hpos[i]) emax = max(emax, run);
+      if (hnum[i]) emax = max(emax, run);
     }
     sh.scan_carry = emax;
   }
   __syncthreads();
   const int fl = max(floorv, sh.scan_carry);
   for (int sb = 0; sb < 256; sb++) {
-    if (!(hsum[sb] | hpos[sb])) continue;
+    if (!hnum[sb]) continue;
     if (hstart[sb] + hpos[sb] < max(sh.e_best + 1, fl)) continue;
-    rbg_segment(sh, list, m, pb + 8, pv | ((uint32_t)sb << bsh), hstart[sb], fl, level + 1, err);
+    rbg_segment(sh, list, m, pb + 8, pv | ((uint32_t)sb << bsh), hstart[sb], fl, level + 1,
+                hnum[sb], err);
   }
 }
 
@@ -854,8 +851,9 @@ __global__ void __launch_bounds__(RBG_NT, RBG_MINB) rscan_big_kernel(RbgArgs a) 
               sh.e_key = sh.e_id = 0u;
             }
             __syncthreads();
-            rbg_segment(sh, L + __ldcg(&a.loff[tr * 256 + bkt]), __ldcg(&a.hcnt[tr * 256 + bkt]), 8,
-                        (uint32_t)bkt << 24, __ldcg(&a.cb[tr * 256 + bkt]), E, 0, a.err);
+            const int mb = __ldcg(&a.hcnt[tr * 256 + bkt]);
+            rbg_segment(sh, L + __ldcg(&a.loff[tr * 256 + bkt]), mb, 8, (uint32_t)bkt << 24,
+                        __ldcg(&a.cb[tr * 256 + bkt]), E, 0, mb, a.err);
             __syncthreads();
             if (tid == 0) {
               int *rb = a.resb + (tr * 256 + bkt) * 4;
