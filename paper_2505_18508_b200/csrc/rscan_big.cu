@@ -245,14 +245,28 @@ __device__ void rbg_segment(RbgShared &sh, const unsigned long long *list, int m
     atomicAdd(&hnum[sb], 1);
   });
   __syncthreads();
-  if (tid == 0) {
-    int run = base, emax = INT_MIN;
-    for (int i = 0; i < 256; i++) {
-      hstart[i] = run;
-      run += hsum[i];
-      if (hnum[i]) emax = max(emax, run);
+  if (tid < 32) {  // sub-bucket starts: 8 per lane, warp scan; candidates as a bit mask
+    int sb8[8], tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      sb8[i] = hsum[tid * 8 + i];
+      tot += sb8[i];
     }
-    sh.scan_carry = emax;
+    int incl = tot;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (tid >= off) incl += y;
+    }
+    int run = base + incl - tot, emax = INT_MIN;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      hstart[tid * 8 + i] = run;
+      run += sb8[i];
+      if (hnum[tid * 8 + i]) emax = max(emax, run);
+    }
+    emax = __reduce_max_sync(0xffffffffu, emax);
+    if (tid == 0) sh.scan_carry = emax;
   }
   __syncthreads();
   const int fl = max(floorv, sh.scan_carry);
