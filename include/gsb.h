@@ -151,6 +151,11 @@ int gsb_test_rscan_shape(int32_t warps, int32_t rows_per_lane);
  * the owning lane, candidate buckets split over passes, ordered extraction). */
 int gsb_test_rscan_limits(int32_t tie_queue_cap, int32_t list_cap);
 
+/* TEST-ONLY: force the number of sweep slices of annealing random-scan launches
+ * (0 = the launcher's choice: slices only when the trials exceed the resident
+ * teams and the schedule is long).  Results never depend on it. */
+int gsb_test_rscan_slices(int32_t slices);
+
 /* Counters of the last random-scan sweep call on this workspace: out4[0] =
  * rounds (summed over trials), [1] sweeps whose best-so-far needed the bucket
  * pass, [2] candidate buckets sorted exactly, [3] top-byte ties resolved by

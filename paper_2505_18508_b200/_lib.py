@@ -90,6 +90,7 @@ def lib():
         L.gsb_test_checker_shape.argtypes = [i32, i32]
         L.gsb_test_cluster_size.argtypes = [i32]
         L.gsb_test_rscan_limits.argtypes = [i32, i32]
+        L.gsb_test_rscan_slices.argtypes = [i32]
         L.gsb_philox_bench.argtypes = [i64, P, P]
         L.gsb_lop3_bench.argtypes = [i64, P, P]
         L.gsb_best_key.argtypes = [P, i32, i64, P, P]

@@ -183,10 +183,12 @@ size_t gsb_torus_workspace_bytes(const gsb_torus *inst, int engine, int32_t swee
   int n = inst->rows * inst->cols;
   size_t b = err_bytes();
   if (engine == GSB_ENGINE_RANDOM_SCAN || engine == GSB_ENGINE_RANDOM_SCAN_LARGE) {
-    // rscan2 needs no scratch beyond the error word and counters; the large-torus
-    // engine keeps the planes of up to 8 trials in the workspace
+    // rscan2 parks trials between sweep slices; the large-torus engine keeps the
+    // planes of up to 8 trials in the workspace
     if (engine == GSB_ENGINE_RANDOM_SCAN_LARGE || !rscan2_fits(inst->rows, inst->cols))
       b += rscan_big_workspace_bytes(inst->rows, inst->cols, T);
+    else
+      b += rscan2_workspace_bytes(inst->rows, inst->cols, T);
   } else if (engine == GSB_ENGINE_CHECKERBOARD && checker_fits(inst->rows, inst->cols)) {
     b += checker_workspace_bytes(inst->rows, inst->cols);
   } else if ((engine == GSB_ENGINE_CHECKERBOARD || engine == GSB_ENGINE_CHECKERBOARD_CLUSTER) &&
@@ -254,7 +256,8 @@ int gsb_torus_sweep(const gsb_torus *inst, int engine, int kind, int32_t sweeps,
     }
   } else if (engine == GSB_ENGINE_RANDOM_SCAN && rscan2_fits(inst->rows, inst->cols)) {
     rc = rscan2_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T, best_cut,
-                    sweeps_exec, best_bits, err, (unsigned long long *)((char *)err + 16), stream);
+                    sweeps_exec, best_bits, rest, err, (unsigned long long *)((char *)err + 16),
+                    stream);
   } else if (engine == GSB_ENGINE_RANDOM_SCAN || engine == GSB_ENGINE_RANDOM_SCAN_LARGE) {
     rc = rscan_big_run(inst->rows, inst->cols, inst->w_dev, kind, sweeps, table, seeds, T,
                        best_cut, sweeps_exec, best_bits, rest, err, stream);
@@ -308,6 +311,12 @@ int gsb_test_rscan_shape(int32_t warps, int32_t rows_per_lane) {
 int gsb_test_rscan_limits(int32_t tie_queue_cap, int32_t list_cap) {
   if (tie_queue_cap < 0 || list_cap < 0) return set_error(GSB_EINVAL, "bad limits");
   rscan2_test_limits(tie_queue_cap, list_cap);
+  return GSB_OK;
+}
+
+int gsb_test_rscan_slices(int32_t slices) {
+  if (slices < 0) return set_error(GSB_EINVAL, "bad slice count");
+  rscan2_force_slices(slices);
   return GSB_OK;
 }
 

@@ -52,9 +52,11 @@ bool rscan2_fits(int rows, int cols);
 bool rscan2_shape(int rows, int cols, int T, int *nw, int *rb);
 void rscan2_force_shape(int nw, int rb);
 void rscan2_test_limits(int tqcap, int lcap);
+void rscan2_force_slices(int nslice);
+size_t rscan2_workspace_bytes(int rows, int cols, int T);
 int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
-               int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws,
+               int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                unsigned long long *stats, cudaStream_t stream);
 
 // random-scan engine for tori beyond rscan2's teams (rscan_big.cu: planes in global memory)

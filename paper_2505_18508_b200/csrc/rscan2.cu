@@ -100,12 +100,14 @@ static int rs2_occupancy(int nw, int rb, bool sa, size_t smem) {
 }
 
 // test-only overrides (gsb_test_rscan_shape, gsb_test_rscan_limits)
-static int g_force_nw = 0, g_force_rb = 0, g_test_tqcap = 0, g_test_lcap = 0;
+static int g_force_nw = 0, g_force_rb = 0, g_test_tqcap = 0, g_test_lcap = 0, g_force_slices = 0;
 
 void rscan2_force_shape(int nw, int rb) {
   g_force_nw = nw;
   g_force_rb = rb;
 }
+
+void rscan2_force_slices(int nslice) { g_force_slices = nslice; }
 
 void rscan2_test_limits(int tqcap, int lcap) {
   g_test_tqcap = tqcap;
@@ -152,6 +154,28 @@ static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupanc
   return found;
 }
 
+// Sweep slices for an annealing launch of T trials on `grid` resident teams
+// (Rs2Args::nslice).  Unsliced, team b runs trials b, b + grid, ...: the launch
+// ends on a part-filled wave (config 2: 1024 trials on 444 seats = 2.31 waves,
+// run as 3) and on the teams whose trials happened to need the most
+// best-so-far work.  Cut into slices drawn from a counter, the seats stay full
+// until the work runs out.  Measured on B200 (tools/slices_ab.py): config 2
+// +18 %, configs 3 / 4 (2000 / 1000 sweeps) +10 % / +8 %, flat from ~13 slices
+// up to slices of 8 sweeps.
+static int rs2_slices(int T, int nsm, const Rs2Shape &sh, int sweeps, bool sa) {
+  if (!sa) return 1;  // greedy trials stop early; nothing to balance
+  if (g_force_slices > 0) return g_force_slices > sweeps ? sweeps : g_force_slices;
+  if ((long long)T <= (long long)nsm * sh.per_sm) return 1;  // a seat per trial
+  const int c = sweeps / 32;
+  return c < 1 ? 1 : c > 16 ? 16 : c;
+}
+
+size_t rscan2_workspace_bytes(int rows, int cols, int T) {
+  const size_t WPR = (size_t)(cols + 31) / 32;
+  const size_t flags = ((size_t)T * 4 + 15) & ~(size_t)15;
+  return flags + (size_t)T * 4 * (4 + 2 * (size_t)rows * WPR);
+}
+
 bool rscan2_fits(int rows, int cols) {
   Rs2Shape sh;
   if (rows < 3 || cols < 3) return false;
@@ -169,7 +193,7 @@ bool rscan2_shape(int rows, int cols, int T, int *nw, int *rb) {
 
 int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
                const uint64_t *table, const uint64_t *seeds, int T, int64_t *best_cut,
-               int32_t *sweeps_exec, uint8_t *best_bits, int *err_ws,
+               int32_t *sweeps_exec, uint8_t *best_bits, void *ws, int *err_ws,
                unsigned long long *stats, cudaStream_t stream) {
   Rs2Shape sh;
   const bool sa = kind == GSB_ANNEALING;
@@ -205,6 +229,19 @@ int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.m_last = 1u << (a.lastvalid - 1);
   a.err = err_ws;
   a.stats = stats;
+  // sweep slices: work counter in the zeroed error block (after the counters),
+  // flags and parked states in the workspace
+  a.nslice = rs2_slices(T, nsm, sh, sweeps, sa);
+  a.slice_len = (sweeps + a.nslice - 1) / a.nslice;
+  a.nslice = (sweeps + a.slice_len - 1) / a.slice_len;
+  a.sl_shift = 0;
+  while ((1LL << a.sl_shift) < T) a.sl_shift++;
+  a.sl_ctr = (uint32_t *)((char *)err_ws + 96);
+  a.sl_flag = (uint32_t *)ws;
+  a.sl_state = (uint32_t *)((char *)ws + (((size_t)T * 4 + 15) & ~(size_t)15));
+  if (a.nslice > 1 &&
+      cudaMemsetAsync(a.sl_flag, 0, (size_t)T * 4, stream) != cudaSuccess)
+    return set_error(GSB_ECUDA, "memset failed");
   const size_t smem = rs2_smem_bytes(sh.NW, sh.RB, rs2_tqcap(a.n), a.nstream);
   const void *kern = rs2_kernel(sh.NW, sh.RB, sa);
   if (!kern) return set_error(GSB_EUNSUPPORTED, "no random-scan kernel for this team shape");

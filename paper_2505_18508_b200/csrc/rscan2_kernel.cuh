@@ -92,6 +92,14 @@ struct Rs2Args {
   // rounds are bound by the ALU pipe, so additions of disjoint bit sets and
   // shifts by these are written as multiply-adds, which issue on the FMA pipe
   uint32_t m_one, m_two, m_neg, m_last;
+  // sweep slices (annealing, more trials than resident teams): the schedule is
+  // cut into nslice pieces of slice_len sweeps and the teams draw (slice, trial)
+  // items slice-major from sl_ctr, so every SM keeps its full set of resident
+  // teams until the work runs out instead of ending on a part-filled wave.  A
+  // trial's spins, best snapshot and cuts wait in sl_state between its slices;
+  // sl_flag[trial] = slices finished.  nslice == 1: trials strided over the grid.
+  int nslice, slice_len, sl_shift;
+  uint32_t *sl_ctr, *sl_flag, *sl_state;
   int *err;
   // [0] rounds, [1] gated sweeps, [2] candidate buckets, [3] ties (queued or inline),
   // [4..9] cycles per phase (GSB_RS2_PROF builds)
@@ -184,6 +192,16 @@ __device__ __forceinline__ void cmp8(const uint32_t *x, const uint32_t *y, uint3
 // the instance's couplings are staged once per CTA)
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// flag hand-over between teams (sweep slices): release store / acquire load at GPU scope
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void tma_bulk_load(void *dst_smem, const void *src_gmem, uint32_t bytes,
@@ -294,6 +312,7 @@ __device__ __forceinline__ void rs2_tie_resolve(uint2 it, const Rs2Tie &c, uint3
   }
   if (prec) atomicOr(f + (kind == 1 ? 2 : 3), 1u << b);
 }
+
 
 // register cap: 14 resident warps per SM (144 registers) for teams of 1-2
 // warps, 16 (128) for larger teams unless 7 rows per lane need more; 8 warps
@@ -445,28 +464,78 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
 
   if (tid == 0) s_misc[6] = 0;
 
-  for (int trial = blockIdx.x; trial < a.T; trial += gridDim.x) {
+  // items: (slice << sl_shift) + trial, 2^sl_shift >= T.  `item` stays a warp-uniform
+  // value for the compiler (block index, kernel arguments, a warp reduction),
+  // so the sweep loop's bounds and branches do
+  const int nitems = a.nslice == 1 ? a.T : a.nslice << a.sl_shift;
+  const int swords = 4 + 2 * rows * WPR;  // sl_state words per trial
+  auto next_item = [&](int item) -> int {
+    if (a.nslice == 1) return item + (int)gridDim.x;
+    if (tid == 0) s_misc[8] = (int)(atomicAdd(a.sl_ctr, 1u) + gridDim.x);
+    team_sync<NW>();
+    return (int)__reduce_max_sync(0xffffffffu, (unsigned)s_misc[8]);
+  };
+  for (int item = blockIdx.x; item < nitems;) {
+    const int slice = item >> a.sl_shift;
+    const int trial = item - (slice << a.sl_shift);
+    if (trial >= a.T) {  // padding of the item space
+      team_sync<NW>();   // s_misc[8] is read by every warp before the next draw
+      item = next_item(item);
+      continue;
+    }
+    const int t_begin = slice * a.slice_len;
+    const int t_end = slice + 1 == a.nslice ? a.sweeps : t_begin + a.slice_len;
     const uint64_t seed = a.seeds[trial];
     const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-    // ---- initial spins: bit b of word 0 of Philox(key, (wi, 0, 31, TAG))
-#pragma unroll
-    for (int j = 0; j < RB; j++) {
-      const uint32_t wi = (uint32_t)(row_of(j) * WPR + c);
-      const P4 o = philox10(P4{wi, 0u, 31u, RS2_TAG}, k0, k1);
-      S[j] = o.x & vslot(j);
-      s_bs[j * NT + tid] = S[j];
-    }
-    s_xtop[par * NT + tid] = make_uint2(S[0], 0u);
-    team_sync<NW>();
     int cur, best, executed = 0;
-    {
-      int c0 = cut_of(S, s_xtop[par * NT + tid_below].x), z1 = 0, z2 = 0, z3 = 0;
-      team_sum4<NW>(s_red, par, lane, warp, c0, z1, z2, z3);
-      cur = best = c0;
+    if (slice == 0) {
+      // ---- initial spins: bit b of word 0 of Philox(key, (wi, 0, 31, TAG))
+#pragma unroll
+      for (int j = 0; j < RB; j++) {
+        const uint32_t wi = (uint32_t)(row_of(j) * WPR + c);
+        const P4 o = philox10(P4{wi, 0u, 31u, RS2_TAG}, k0, k1);
+        S[j] = o.x & vslot(j);
+        s_bs[j * NT + tid] = S[j];
+      }
+      s_xtop[par * NT + tid] = make_uint2(S[0], 0u);
+      team_sync<NW>();
+      {
+        int c0 = cut_of(S, s_xtop[par * NT + tid_below].x), z1 = 0, z2 = 0, z3 = 0;
+        team_sum4<NW>(s_red, par, lane, warp, c0, z1, z2, z3);
+        cur = best = c0;
+      }
+      par ^= 1;
+    } else {
+      // ---- resume: the trial's previous slice (any team) has published its state
+      // (every warp polls for itself: one broadcast load, exit by vote)
+      while (!__all_sync(0xffffffffu, ld_acquire_u32(a.sl_flag + trial) >= (uint32_t)slice))
+        __nanosleep(256);
+      const uint32_t *st = a.sl_state + (size_t)trial * swords;
+      // (broadcast through shared memory like team_sum4's results: the sweep
+      // loop branches on cur and best, and read per thread from global memory
+      // the compiler treats them as divergent values -- the branches and all the
+      // code behind them leave the uniform datapath: +46 % instructions, configs
+      // 3 and 4 a third slower)
+      if (tid == 0) {
+        s_misc[9] = (int)__ldcg(st);
+        s_misc[10] = (int)__ldcg(st + 1);
+        s_misc[11] = (int)__ldcg(st + 2);
+      }
+      team_sync<NW>();
+      cur = s_misc[9];
+      best = s_misc[10];
+      executed = s_misc[11];
+#pragma unroll
+      for (int j = 0; j < RB; j++) {
+        const bool real = act && j < nr;
+        const int wi = real ? (start + j) * WPR + c : 0;
+        const uint2 sb = __ldcg(reinterpret_cast<const uint2 *>(st + 4 + 2 * wi));
+        S[j] = real ? sb.x : 0u;
+        s_bs[j * NT + tid] = real ? sb.y : 0u;
+      }
     }
-    par ^= 1;
 
-    for (int t = 0; t < a.sweeps; t++) {
+    for (int t = t_begin; t < t_end; t++) {
       RS2_TICK(5);
       // ---- per-sweep constants (uniform over the team)
       uint32_t u1q[4], vq[4];
@@ -1078,6 +1147,27 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
       RS2_TICK(4);
     }
 
+    if (slice + 1 < a.nslice) {
+      // ---- park the trial for its next slice
+      uint32_t *st = a.sl_state + (size_t)trial * swords;
+      if (tid == 0) {
+        st[0] = (uint32_t)cur;
+        st[1] = (uint32_t)best;
+        st[2] = (uint32_t)executed;
+      }
+#pragma unroll
+      for (int j = 0; j < RB; j++)
+        if (act && j < nr) {
+          const int wi = (start + j) * WPR + c;
+          *reinterpret_cast<uint2 *>(st + 4 + 2 * wi) = make_uint2(S[j], s_bs[j * NT + tid]);
+        }
+      __threadfence();
+      team_sync<NW>();
+      if (tid == 0) st_release_u32(a.sl_flag + trial, (uint32_t)(slice + 1));
+      item = next_item(item);
+      continue;
+    }
+
     // ---- integrity guard (solvers.py:132-133) and outputs
     uint32_t B[RB];
 #pragma unroll
@@ -1112,6 +1202,7 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
     for (int i = tid; i < a.nbytes; i += NT)
       out[i] = (uint8_t)(s_stream[i >> 2] >> (24 - 8 * (i & 3)));
     team_sync<NW>();
+    item = next_item(item);
   }
   if (a.stats) {
     st_rounds = tid == 0 ? st_rounds : 0;

@@ -214,6 +214,11 @@ def _test_rscan_limits(tie_queue_cap: int = 0, list_cap: int = 0) -> None:
     _lib.check(_lib.lib().gsb_test_rscan_limits(tie_queue_cap, list_cap))
 
 
+def _test_rscan_slices(slices: int = 0) -> None:
+    """TEST-ONLY: force the sweep slices of annealing random-scan launches (0 = automatic)."""
+    _lib.check(_lib.lib().gsb_test_rscan_slices(slices))
+
+
 def run_trials_device(instance: ProblemInstance, config: SolverConfig, seeds, device=None,
                       stream=None, check: bool = True, engine: int | None = None):
     """Batched trials with device-resident outputs (torch tensors).

@@ -42,6 +42,7 @@ from paper_2505_18508_b200.solvers import (  # noqa: E402
     default_config,
     _test_rscan_limits,
     _test_rscan_shape,
+    _test_rscan_slices,
     rscan_shape,
     run_trials,
     run_trials_device,
@@ -116,6 +117,49 @@ def test_random_scan_overflow_paths(oracle, tq, lc):
             _check(oracle, inst, SolverConfig(ANNEALING_RANDOM_SCAN, 6, 0, 0.9, 0.3), seeds)
     finally:
         _test_rscan_limits(0, 0)
+
+
+@pytest.mark.parametrize("slices", [2, 3, 7, 40])
+def test_random_scan_sweep_slices(oracle, slices):
+    """Sweep slices (teams draw (slice, trial) items; a trial's state waits in
+    the workspace between its slices): the oracle's results at any slice
+    count, with fewer trials than teams, more, and team shapes with dummy rows."""
+    try:
+        _test_rscan_slices(slices)
+        for (R, C, s, T) in [(9, 11, 4, 5), (40, 33, 7, 700), (50, 100, 1, 1000),
+                             (100, 100, 1, 1500)]:
+            inst = generate_torus(TorusSpec(R, C, s))
+            seeds = mix_seeds(MASTER, range(T))
+            idx = sorted(set(np.linspace(0, T - 1, 12).astype(int).tolist()))
+            _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, 40, 0), seeds, idx)
+            _check(oracle, inst, SolverConfig(ANNEALING_RANDOM_SCAN, 7, 0, 0.9, 0.3), seeds, idx)
+        for shape in [(4, 4), (8, 2), (2, 7)]:
+            try:
+                _test_rscan_shape(*shape)
+                inst = generate_torus(TorusSpec(50, 100, 1))
+                seeds = mix_seeds(MASTER, range(600))
+                _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, 30, 0), seeds,
+                       [0, 1, 299, 598, 599])
+            finally:
+                _test_rscan_shape(0, 0)
+    finally:
+        _test_rscan_slices(0)
+
+
+def test_random_scan_sweep_slices_automatic():
+    """The launcher slices config 2's own launch (1024 trials on 444 resident
+    teams, 10 000 sweeps): identical results to the unsliced launch."""
+    inst = generate_torus(TorusSpec(100, 100, 1))
+    seeds = mix_seeds(20250814, range(1024))
+    cfg = default_config(ANNEALING_RANDOM_SCAN, 1200, 0)
+    auto = run_trials(inst, cfg, seeds)
+    try:
+        _test_rscan_slices(1)
+        one = run_trials(inst, cfg, seeds)
+    finally:
+        _test_rscan_slices(0)
+    assert np.array_equal(np.asarray(auto.best_cut), np.asarray(one.best_cut))
+    assert [auto.hex(i) for i in (0, 500, 1023)] == [one.hex(i) for i in (0, 500, 1023)]
 
 
 @pytest.mark.parametrize("R,C,T,S", [(50, 100, 100, 200), (100, 100, 1024, 60),
