@@ -216,9 +216,11 @@ def python_reference_rate(rows, cols, seconds_target=8.0):
     """The unmodified Python reference (baseline/_ref copy of gsetbench, made by
     __graft_entry__.build()) on all host cores: ProcessPoolExecutor(P), one
     run_trial per process, sweeps bounded to ~seconds_target.
-    Returns None when the copy is absent."""
+    Returns None when the copy is absent, and beyond 10^5 sites (config 5: the
+    reference builds 8e6 edges as Python objects in each of the P processes --
+    minutes and tens of GB before the first sweep; the C port stands alone there)."""
     src = ROOT / "baseline" / "_ref" / "pkg" / "src"
-    if not (src / "gsetbench" / "solvers.py").exists():
+    if not (src / "gsetbench" / "solvers.py").exists() or rows * cols > 100_000:
         return None
     from concurrent.futures import ProcessPoolExecutor
 
@@ -348,7 +350,8 @@ def main(argv=None):
     from paper_2505_18508_b200.campaign import mix_seeds
     from paper_2505_18508_b200.distributed import reduce_best as reduce_best_dist
     from paper_2505_18508_b200.solvers import (CHECKERBOARD_KINDS, RANDOM_SCAN_KINDS,
-                                               default_config, run_trials_device, schedule_table)
+                                               default_config, rscan_shape, run_trials_device,
+                                               schedule_table)
 
     if not share and torch.cuda.device_count() < (local + 1):
         print(f"bench.py: rank {rank} needs cuda:{local} but only {torch.cuda.device_count()} "
@@ -609,8 +612,13 @@ def main(argv=None):
         roofline = {
             "bound": "int", "unit": "Tops/s (ALU-pipe integer thread operations: LOP3/SHF)",
             "achieved": alu_ops / launch_s / 1e12, "peak": lop3_peak / 1e12,
-            "frac": alu_ops / launch_s / lop3_peak, "traffic": None,
+            "frac": alu_ops / launch_s / lop3_peak,
+            # DRAM bytes of one launch at config 2 from the committed ncu capture (the
+            # planes live in registers / shared memory: HBM sees couplings, seeds, results)
+            "traffic": 610304 if (rows, cols, T, S) == (100, 100, 1024, 10000) else None,
             "kernel": sweep_kernel,
+            "team_shape": dict(zip(("warps_per_trial", "rows_per_lane"),
+                                   rscan_shape(rows, cols, T))),
             "algorithmic_units_per_launch": alu_ops,
             "unit_def": f"{fixed} + {per_round} x rounds ALU-pipe operations per 32-site word and "
                         "sweep: what the contract's level-synchronous bit-sliced algorithm needs "
@@ -623,11 +631,11 @@ def main(argv=None):
             "updates_per_launch": upd_rank, "launch_ms": launch_s * 1e3,
             "updates_per_s": kernel_rate, "philox": philox_roof, "smem": smem,
             # not measured by this run: the committed ncu capture of the same launch
-            "ncu_capture": {"file": "profiles/r02_ncu_rscan2_v5_summary.txt",
+            "ncu_capture": {"file": "profiles/r02_ncu_rscan2_v7_summary.txt",
                             "workload": "config 2, 1024 trials x 10000 sweeps, rscan2_kernel<7,2>",
-                            "alu_pipe_active_pct": 55.4, "fma_pipe_active_pct": 15.5,
-                            "ipc_per_sm": 2.20, "issue_active_pct": 55.2,
-                            "warp_instructions_per_update": 2.0, "dram_bytes": 606208},
+                            "alu_pipe_active_pct": 58.6, "fma_pipe_active_pct": 17.4,
+                            "ipc_per_sm": 2.37, "issue_active_pct": 59.4,
+                            "warp_instructions_per_update": 2.08, "dram_bytes": 610304},
         }
     elif blocks_per_step is not None:
         roofline = {
