@@ -146,6 +146,45 @@ def test_random_scan_sweep_slices(oracle, slices):
         _test_rscan_slices(0)
 
 
+def test_random_scan_sweep_slices_concurrent_streams():
+    """Sliced launches from three host threads on their own streams at once:
+    teams of different launches share the SMs while they poll each other's
+    launch-private flags; every launch returns what it returns alone."""
+    import threading
+
+    import torch
+
+    jobs = [((100, 100), 700, 40), ((50, 100), 900, 50), ((40, 33), 1500, 60)]
+    ref, bad = [], []
+    try:
+        _test_rscan_slices(5)
+        for (R, C), T, S in jobs:
+            inst = generate_torus(TorusSpec(R, C, 1))
+            cfg = default_config(ANNEALING_RANDOM_SCAN, S, 0)
+            b = run_trials_device(inst, cfg, mix_seeds(7, range(T)))
+            ref.append((inst, cfg, T, b[0].cpu().numpy().copy(), b[2].cpu().numpy().copy()))
+        torch.cuda.synchronize()
+
+        def work(k):
+            st = torch.cuda.Stream()
+            for r in range(3):
+                inst, cfg, T, cuts, bits = ref[(k + r) % len(ref)]
+                b = run_trials_device(inst, cfg, mix_seeds(7, range(T)), stream=st)
+                st.synchronize()
+                if not (np.array_equal(b[0].cpu().numpy(), cuts)
+                        and np.array_equal(b[2].cpu().numpy(), bits)):
+                    bad.append((k, r))
+
+        ths = [threading.Thread(target=work, args=(k,)) for k in range(3)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    finally:
+        _test_rscan_slices(0)
+    assert not bad
+
+
 def test_random_scan_sweep_slices_automatic():
     """The launcher slices config 2's own launch (1024 trials on 444 resident
     teams, 10 000 sweeps): identical results to the unsliced launch."""

@@ -8,7 +8,7 @@ sys.path.insert(0, '.')
 from oracle import oracle as O
 from paper_2505_18508_b200 import TorusSpec, _lib, generate_torus
 from paper_2505_18508_b200.solvers import (SolverConfig, _test_rscan_limits, _test_rscan_shape,
-                                           rscan_fits, run_trials)
+                                           _test_rscan_slices, rscan_fits, run_trials)
 
 O.build()
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
@@ -35,6 +35,8 @@ for it in range(cases):
     if rng.random() < 0.5:
         forced = (int(rng.choice([1, 2, 4, 7, 8])), int(rng.choice([1, 2, 3, 4, 5, 7])))
     _test_rscan_shape(*forced)
+    slices = int(rng.choice([0, 0, 1, 2, 3, 5, 64]))  # sweep slices of annealing launches
+    _test_rscan_slices(slices)
     eng = _lib.ENGINE_RANDOM_SCAN_LARGE if rng.random() < 0.3 else None  # the large-torus engine
     if eng is not None:
         forced = ("large",)
