@@ -316,12 +316,17 @@ __device__ __forceinline__ void rs2_tie_resolve(uint2 it, const Rs2Tie &c, uint3
 
 // register cap: 14 resident warps per SM (144 registers) for teams of 1-2
 // warps, 16 (128) for larger teams unless 7 rows per lane need more; 8 warps
-// x 2 rows run 24 warps per SM at 80 registers (config 2: +10 % over 4 x 4 at
-// 128; lower caps for the other shapes only spill, profiles/r02_rscan2_regcaps.txt)
+// x 2 rows run 24 warps per SM at 80 registers, and 7 x 2 (config 2) four
+// teams = 28 warps per SM at 72: with sweep slices keeping every seat busy the
+// fourth team is worth +7 % over three at 80 (before the slices it was not;
+// 96 for 4 x 5, 7 x 3, 7 x 4 buys a team more per SM and loses 4-13 % to
+// spills: profiles/r02_rscan2_regcaps.txt, r02_rscan2_regcaps_sliced.txt)
 constexpr int rs2_max_regs(int NW, int RB) {
   return NW <= 2 ? 144
-                 : NW == 4 ? (RB >= 7 ? 168 : 128)
-                           : (RB >= 7 ? 255 : RB == 2 ? 80 : 128);  // 7 or 8 warps
+         : NW == 4 ? (RB >= 7 ? 168 : 128)
+         : RB >= 7 ? 255
+         : RB == 2 ? (NW == 7 ? 72 : 80)
+                   : 128;  // 7 or 8 warps
 }
 
 template <int NW, int RB, bool SA>
