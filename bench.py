@@ -615,7 +615,7 @@ def main(argv=None):
             "frac": alu_ops / launch_s / lop3_peak,
             # DRAM bytes of one launch at config 2 from the committed ncu capture (the
             # planes live in registers / shared memory: HBM sees couplings, seeds, results)
-            "traffic": 610304 if (rows, cols, T, S) == (100, 100, 1024, 10000) else None,
+            "traffic": 857344 if (rows, cols, T, S) == (100, 100, 1024, 10000) else None,
             "kernel": sweep_kernel,
             "team_shape": dict(zip(("warps_per_trial", "rows_per_lane"),
                                    rscan_shape(rows, cols, T))),
@@ -631,11 +631,11 @@ def main(argv=None):
             "updates_per_launch": upd_rank, "launch_ms": launch_s * 1e3,
             "updates_per_s": kernel_rate, "philox": philox_roof, "smem": smem,
             # not measured by this run: the committed ncu capture of the same launch
-            "ncu_capture": {"file": "profiles/r02_ncu_rscan2_v7_summary.txt",
+            "ncu_capture": {"file": "profiles/r02_ncu_rscan2_v8_summary.txt",
                             "workload": "config 2, 1024 trials x 10000 sweeps, rscan2_kernel<7,2>",
-                            "alu_pipe_active_pct": 58.6, "fma_pipe_active_pct": 17.4,
-                            "ipc_per_sm": 2.37, "issue_active_pct": 59.4,
-                            "warp_instructions_per_update": 2.08, "dram_bytes": 610304},
+                            "alu_pipe_active_pct": 63.0, "fma_pipe_active_pct": 18.4,
+                            "ipc_per_sm": 2.57, "issue_active_pct": 64.6,
+                            "warp_instructions_per_update": 2.11, "dram_bytes": 857344},
         }
     elif blocks_per_step is not None:
         roofline = {
