@@ -234,6 +234,7 @@ int rscan2_run(int rows, int cols, const int8_t *w_dev, int kind, int sweeps,
   a.nslice = rs2_slices(T, nsm, sh, sweeps, sa);
   a.slice_len = (sweeps + a.nslice - 1) / a.nslice;
   a.nslice = (sweeps + a.slice_len - 1) / a.slice_len;
+  a.dynamic = a.nslice > 1 || (long long)T > (long long)nsm * sh.per_sm;
   a.sl_shift = 0;
   while ((1LL << a.sl_shift) < T) a.sl_shift++;
   a.sl_ctr = (uint32_t *)((char *)err_ws + 96);

@@ -97,8 +97,9 @@ struct Rs2Args {
   // items slice-major from sl_ctr, so every SM keeps its full set of resident
   // teams until the work runs out instead of ending on a part-filled wave.  A
   // trial's spins, best snapshot and cuts wait in sl_state between its slices;
-  // sl_flag[trial] = slices finished.  nslice == 1: trials strided over the grid.
+  // sl_flag[trial] = slices finished.  Greedy launches draw whole trials (nslice == 1).
   int nslice, slice_len, sl_shift;
+  int dynamic;  // items drawn from sl_ctr (more trials than teams); else strided over the grid
   uint32_t *sl_ctr, *sl_flag, *sl_state;
   int *err;
   // [0] rounds, [1] gated sweeps, [2] candidate buckets, [3] ties (queued or inline),
@@ -475,7 +476,7 @@ unsigned long long st_rounds = 0, st_gated = 0, st_cand = 0, st_ties = 0;
   const int nitems = a.nslice == 1 ? a.T : a.nslice << a.sl_shift;
   const int swords = 4 + 2 * rows * WPR;  // sl_state words per trial
   auto next_item = [&](int item) -> int {
-    if (a.nslice == 1) return item + (int)gridDim.x;
+    if (!a.dynamic) return item + (int)gridDim.x;
     if (tid == 0) s_misc[8] = (int)(atomicAdd(a.sl_ctr, 1u) + gridDim.x);
     team_sync<NW>();
     return (int)__reduce_max_sync(0xffffffffu, (unsigned)s_misc[8]);
