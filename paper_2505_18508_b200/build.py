@@ -16,7 +16,7 @@ LIB = PKG / "libgsb_cuda.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["abi.cu", "checker.cu", "checker_hbm.cu", "checker_cluster.cu", "refexact.cu", "refexact_warp.cu",
-           "evaluate.cu", "rscan2.cu", "rscan2_nw1.cu", "rscan2_nw2.cu", "rscan2_nw4.cu", "rscan2_nw7.cu", "rscan2_nw8.cu", "rscan_big.cu"]
+           "evaluate.cu", "rscan2.cu", "rscan2_nw1.cu", "rscan2_nw2.cu", "rscan2_nw4.cu", "rscan2_nw7.cu", "rscan2_nw8.cu", "rscan2_nw9.cu", "rscan2_nw13.cu", "rscan_big.cu"]
 HEADERS = ["gsb_device.cuh", "gsb_internal.h", "checker_common.cuh", "rscan2_kernel.cuh"]
 
 NVCC_FLAGS = [

@@ -1,10 +1,12 @@
 // rscan2.cu -- random-scan engine (kinds *_random_scan): host side.
 //
 // Team shape selection and launch of rscan2_kernel<NW, RB, SA>
-// (rscan2_kernel.cuh has the algorithm; rscan2_nw{1,2,4,7,8}.cu the
+// (rscan2_kernel.cuh has the algorithm; rscan2_nw{1,2,4,7,8,9,13}.cu the
 // instantiations).  NW warps per trial in {1, 2, 4, 7, 8}, RB rows per lane in
 // {1, 2, 3, 4, 5, 7}: a torus fits when rows <= NW * floor(32 / WPR) * RB for
-// some shape, WPR = ceil(cols / 32) <= 32.
+// some shape, WPR = ceil(cols / 32) <= 32; teams of 9 and 13 warps with at most
+// two rows per lane add occupancy for 100-row tori of 5 and 7 words per row
+// (configs 3 and 4), never reach.
 #include <cuda_runtime.h>
 
 #include <mutex>
@@ -18,7 +20,7 @@ struct Rs2Shape {
 };
 
 static const int kRbSet[] = {1, 2, 3, 4, 5, 7};
-static const int kNwSet[] = {1, 2, 4, 7, 8};
+static const int kNwSet[] = {1, 2, 4, 7, 8, 9, 13};
 
 static const void *rs2_kernel(int nw, int rb, bool sa) {
   switch (nw) {
@@ -32,6 +34,10 @@ static const void *rs2_kernel(int nw, int rb, bool sa) {
       return rs2_kernel_nw7(rb, sa);
     case 8:
       return rs2_kernel_nw8(rb, sa);
+    case 9:
+      return rs2_kernel_nw9(rb, sa);
+    case 13:
+      return rs2_kernel_nw13(rb, sa);
     default:
       return nullptr;
   }
@@ -123,7 +129,7 @@ void rscan2_test_limits(int tqcap, int lcap) {
 // device): only feasibility, first fit.
 static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupancy, Rs2Shape &sh) {
   const int WPR = (cols + 31) / 32;
-  if (WPR > 32) return false;
+  if (WPR > 32 || rows * WPR > 2048) return false;  // tie items carry 11-bit word indices
   const int BPW = 32 / WPR;
   const int n = rows * cols, nstream = (n + 31) / 32, tqcap = rs2_tqcap(n);
   bool found = false;
@@ -131,6 +137,7 @@ static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupanc
   for (int nw : kNwSet) {
     for (int RB : kRbSet) {
       if (occupancy && g_force_nw > 0 && (nw != g_force_nw || RB != g_force_rb)) continue;
+      if (nw > 8 && (RB > 2 || !occupancy)) continue;  // wide teams: two rows per lane at most
       int NBu, nbig;
       if (!rs2_blocks(rows, RB, nw * BPW, NBu, nbig)) continue;
       if (!occupancy) {
@@ -141,7 +148,8 @@ static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupanc
       if (per_sm < 1) continue;
       const long long tps = ((long long)T + nsm - 1) / nsm;  // trials per SM
       const long long full = tps / per_sm, rem = tps % per_sm;
-      const double bar = 1.0 + 0.03 * (nw == 1 ? 0 : nw == 2 ? 1 : nw == 4 ? 2 : 3);  // ~log2 NW
+      const double bar =
+          1.0 + 0.03 * (nw == 1 ? 0 : nw == 2 ? 1 : nw == 4 ? 2 : nw <= 9 ? 3 : 3.7);  // ~log2 NW
       auto wave = [&](long long k) { return (double)RB * ((double)k * nw + 12.0) * bar; };
       const double cost = (double)full * wave(per_sm) + (rem ? wave(rem) : 0.0);
       if (!found || cost < bestcost - 1e-9) {

@@ -326,8 +326,8 @@ constexpr int rs2_max_regs(int NW, int RB) {
   return NW <= 2 ? 144
          : NW == 4 ? (RB >= 7 ? 168 : 128)
          : RB >= 7 ? 255
-         : RB == 2 ? (NW == 7 ? 72 : 80)
-                   : 128;  // 7 or 8 warps
+         : RB == 2 ? (NW == 8 ? 80 : 72)
+                   : 128;  // 7 warps and more
 }
 
 template <int NW, int RB, bool SA>
@@ -1232,6 +1232,8 @@ const void *rs2_kernel_nw2(int rb, bool sa);
 const void *rs2_kernel_nw4(int rb, bool sa);
 const void *rs2_kernel_nw7(int rb, bool sa);
 const void *rs2_kernel_nw8(int rb, bool sa);
+const void *rs2_kernel_nw9(int rb, bool sa);
+const void *rs2_kernel_nw13(int rb, bool sa);
 
 #define RS2_DEFINE_TABLE(NWV)                                                   \
   const void *rs2_kernel_nw##NWV(int rb, bool sa) {                             \
@@ -1254,6 +1256,22 @@ const void *rs2_kernel_nw8(int rb, bool sa);
       case 7:                                                                   \
         return sa ? (const void *)rscan2_kernel<NWV, 7, true>                   \
                   : (const void *)rscan2_kernel<NWV, 7, false>;                 \
+      default:                                                                  \
+        return nullptr;                                                         \
+    }                                                                           \
+  }
+
+// teams beyond 8 warps exist for two rows per lane only (more rows per lane
+// would not fit the register file at these team sizes)
+#define RS2_DEFINE_TABLE_WIDE(NWV)                                              \
+  const void *rs2_kernel_nw##NWV(int rb, bool sa) {                             \
+    switch (rb) {                                                               \
+      case 1:                                                                   \
+        return sa ? (const void *)rscan2_kernel<NWV, 1, true>                   \
+                  : (const void *)rscan2_kernel<NWV, 1, false>;                 \
+      case 2:                                                                   \
+        return sa ? (const void *)rscan2_kernel<NWV, 2, true>                   \
+                  : (const void *)rscan2_kernel<NWV, 2, false>;                 \
       default:                                                                  \
         return nullptr;                                                         \
     }                                                                           \

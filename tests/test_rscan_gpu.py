@@ -82,9 +82,9 @@ def test_random_scan_every_team_shape(oracle):
     """Every (warps, rows per lane) instantiation, forced through the
     test-only shape override on tori that fill it, against the oracle."""
     try:
-        for nw in (1, 2, 4, 7, 8):
-            for rb in (1, 2, 3, 4, 5, 7):
-                for C in (200, 100, 33):  # 7 / 4 / 2 words per row (4, 4 and 1 valid bits in the last)
+        for nw in (1, 2, 4, 7, 8, 9, 13):
+            for rb in (1, 2, 3, 4, 5, 7) if nw <= 8 else (1, 2):  # wide teams: <= 2 rows
+                for C in (200, 140, 100, 33):  # 7 / 5 / 4 / 2 words per row (8, 12, 4 and 1 valid bits in the last)
                     bpw = 32 // ((C + 31) // 32)
                     R = nw * bpw * rb - (1 if rb > 1 else 0)
                     if R * C > 30000:
@@ -209,7 +209,7 @@ def test_random_scan_benchmark_shapes(oracle, R, C, T, S):
     inst = generate_torus(TorusSpec(R, C, 1))
     seeds = mix_seeds(20250814, range(T))
     idx = sorted(set(np.linspace(0, T - 1, 16).astype(int).tolist()))
-    assert rscan_shape(R, C, T)[0] in (1, 2, 4, 7, 8)
+    assert rscan_shape(R, C, T)[0] in (1, 2, 4, 7, 8, 9, 13)
     _check(oracle, inst, default_config(ANNEALING_RANDOM_SCAN, S, 0), seeds, idx)
     _check(oracle, inst, default_config(GREEDY_RANDOM_SCAN, 200, 0), seeds, idx)
 

@@ -33,7 +33,7 @@ for it in range(cases):
     _test_rscan_limits(*lim)
     forced = (0, 0)
     if rng.random() < 0.5:
-        forced = (int(rng.choice([1, 2, 4, 7, 8])), int(rng.choice([1, 2, 3, 4, 5, 7])))
+        forced = (int(rng.choice([1, 2, 4, 7, 8, 9, 13])), int(rng.choice([1, 2, 3, 4, 5, 7])))
     _test_rscan_shape(*forced)
     slices = int(rng.choice([0, 0, 1, 2, 3, 5, 64]))  # sweep slices of annealing launches
     _test_rscan_slices(slices)
