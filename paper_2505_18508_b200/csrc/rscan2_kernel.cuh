@@ -1,6 +1,6 @@
 // rscan2_kernel.cuh -- random-scan engine (kinds *_random_scan), contract v2:
 // the kernel template.  Host side and shape selection: rscan2.cu; the
-// instantiations are spread over rscan2_nw{1,2,4,7,8}.cu to compile in parallel.
+// instantiations are spread over rscan2_nw{1,2,4,7,8,9,13}.cu to compile in parallel.
 //
 // The reference sweep (solvers.py:107-127) visits every site once in a fresh
 // uniformly random order and updates it from its current neighbours.  Here
