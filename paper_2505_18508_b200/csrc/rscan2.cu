@@ -4,7 +4,7 @@
 // (rscan2_kernel.cuh has the algorithm; rscan2_nw{1,2,4,7,8,9,13}.cu the
 // instantiations).  NW warps per trial in {1, 2, 4, 7, 8}, RB rows per lane in
 // {1, 2, 3, 4, 5, 7}: a torus fits when rows <= NW * floor(32 / WPR) * RB for
-// some shape, WPR = ceil(cols / 32) <= 32; teams of 9 and 13 warps with at most
+// some shape, WPR = ceil(cols / 32) <= 32; teams of 9 and 13 warps with
 // two rows per lane add occupancy for 100-row tori of 5 and 7 words per row
 // (configs 3 and 4), never reach.
 #include <cuda_runtime.h>
@@ -137,7 +137,7 @@ static bool rs2_shape(int rows, int cols, int T, int nsm, bool sa, bool occupanc
   for (int nw : kNwSet) {
     for (int RB : kRbSet) {
       if (occupancy && g_force_nw > 0 && (nw != g_force_nw || RB != g_force_rb)) continue;
-      if (nw > 8 && (RB > 2 || !occupancy)) continue;  // wide teams: two rows per lane at most
+      if (nw > 8 && (RB != 2 || !occupancy)) continue;  // wide teams: two rows per lane only
       int NBu, nbig;
       if (!rs2_blocks(rows, RB, nw * BPW, NBu, nbig)) continue;
       if (!occupancy) {

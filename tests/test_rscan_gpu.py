@@ -83,7 +83,7 @@ def test_random_scan_every_team_shape(oracle):
     test-only shape override on tori that fill it, against the oracle."""
     try:
         for nw in (1, 2, 4, 7, 8, 9, 13):
-            for rb in (1, 2, 3, 4, 5, 7) if nw <= 8 else (1, 2):  # wide teams: <= 2 rows
+            for rb in (1, 2, 3, 4, 5, 7) if nw <= 8 else (2,):  # wide teams: 2 rows per lane
                 for C in (200, 140, 100, 33):  # 7 / 5 / 4 / 2 words per row (8, 12, 4 and 1 valid bits in the last)
                     bpw = 32 // ((C + 31) // 32)
                     R = nw * bpw * rb - (1 if rb > 1 else 0)
